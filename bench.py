@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""bench.py -- the arXiv 1312.1869 hot path on B200: sketch Y = K Omega -> TSQR -> low-rank solve.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One "step" = one pass of the whole hot path over the
+config's synthetic input: sketch randomness + fused covariance/SRHT sketch,
+blocked TSQR with explicit Q, Q^T A, truncated back substitution, X = Omega Z.
+N > 1 (torchrun): rows are sharded, R factors all-gathered (NCCL), C all-reduced.
+
+Metric (BASELINE.json): "K Omega sketch throughput (n^2 d/s) and end-to-end TSQR
+low-rank solve time vs n".  `value` = n^2 d / (max-over-ranks step time), i.e.
+nominal dense-equivalent n^2 d per second of the WHOLE step; the sketch-only
+throughput and the per-phase / end-to-end times are reported beside it.
+Timing: CUDA events per step on the launching stream; L2 flushed (a 256 MiB write)
+between timed steps outside the events; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ks_inputs  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_SM_MHZ = 1965.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto, ~10-20 s)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ algorithmic work
+def alu_ops_per_element(cfg) -> float:
+    """Algorithmic FP32 ops per K element of the fused SRHT sketch:
+    SE 2D+2, Matern-3/2 2D+4 (sign folded into the amplitude), + (N/n) log2 d transform adds."""
+    D = cfg["dim"]
+    kern = 2 * D + 2 if cfg["kernel"] == ks_inputs.SQEXP else 2 * D + 4
+    n = cfg["n"]
+    N = 1 << (n - 1).bit_length()
+    return kern + (N / n) * np.log2(cfg["d"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ oracle leg (cpu_baseline / --impl reference)
+def oracle_sample(cfg, pts, rows_hint=0, budget_s=12.0):
+    """Time the oracle (as it stands) on a bounded row sample of the sketch; returns
+    (n2d_per_s, rows, seconds, threads)."""
+    import oracle
+    prob = oracle.Problem.from_cfg(cfg, pts)
+    _ = prob.s, prob.S  # randomness (excluded, like the GPU's setup)
+    threads = oracle._threads()
+    n, d = cfg["n"], cfg["d"]
+    if rows_hint:
+        rows = rows_hint
+    else:  # calibrate on a small sample, then size it to ~budget_s
+        probe = max(threads, 8)
+        t0 = time.perf_counter()
+        prob.sketch_rows(np.arange(probe, dtype=np.int64))
+        dt = time.perf_counter() - t0
+        rows = int(max(probe, min(n, probe * budget_s / max(dt, 1e-3))))
+        rows = max(threads, (rows // threads) * threads)
+    sel = np.linspace(0, n - 1, rows).astype(np.int64)
+    t0 = time.perf_counter()
+    prob.sketch_rows(sel)
+    dt = time.perf_counter() - t0
+    return rows * n * d / dt, rows, dt, threads
+
+
+def run_reference(args, cfg, pts):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    rate, rows, dt, threads = oracle_sample(cfg, pts, args.cpu_rows)
+    per_step_rows = rows
+    times = []
+    import oracle
+    prob = oracle.Problem.from_cfg(cfg, pts)
+    sel = np.linspace(0, cfg["n"] - 1, per_step_rows).astype(np.int64)
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state worth amortising
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        prob.sketch_rows(sel)
+        times.append(time.perf_counter() - t0)
+    n, d = cfg["n"], cfg["d"]
+    v = per_step_rows * n * d / statistics.mean(times)
+    sample = f"oracle tier-B sketch (fp64 C, {threads} threads) of {per_step_rows} evenly spaced rows of {args.config}; TSQR/solve not in the sample"
+    print(json.dumps({
+        "impl": "reference", "metric": "K Omega sketch throughput (n^2 d/s), end-to-end low-rank solve",
+        "value": v, "unit": "n^2*d/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "d": d, "sample_rows": per_step_rows},
+        "cpu_baseline": {"value": v, "unit": "n^2*d/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "n^2*d/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg, pts_np, A_np):
+    import torch
+    import torch.distributed as dist
+    import paper_1312_1869_b200 as ks
+    from paper_1312_1869_b200 import dist as ksd
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    n, d, m = cfg["n"], cfg["d"], cfg["m"]
+    blocks = cfg["blocks"]  # per GPU for c4/c5 ("blocks_per_gpu"), else split evenly
+    if not cfg.get("blocks_per_gpu"):
+        blocks = max(1, blocks // world)
+    rb, re = ksd.shard_rows(n, world, rank)
+    desc = dict(n=n, dim=cfg["dim"], kernel=cfg["kernel"], sigma2=cfg["sigma2"], ell=cfg["ell"],
+                nugget=cfg["nugget"], d=d, seed=cfg["seed"], omega=cfg["omega"])
+    ops = ksd.CudaOps(desc, m, blocks, 1e-5, rank, world, dev)
+    pts = torch.as_tensor(pts_np, device=dev)
+    A_loc = torch.as_tensor(np.ascontiguousarray(A_np[rb:re]), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def step():
+        ksd.lowrank_solve_sharded(ops, pts, A_loc)
+
+    # phase events (one step, after warm-up) and per-step events (timed region)
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    sk_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    launches0 = ks.lib().ks_launch_count() if hasattr(ks.lib(), "ks_launch_count") else None
+    with ClockSampler(dev.index) as clk:
+        barrier()
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)  # L2 flush outside the timed events
+            ev[2 * s].record(stream)
+            sk_ev[2 * s].record(stream)
+            Y = ops.sketch(pts)
+            sk_ev[2 * s + 1].record(stream)
+            Rp = ops.local_r(Y)
+            if world > 1:
+                Rstack = torch.empty((world * d, d), dtype=torch.float32, device=dev)
+                dist.all_gather_into_tensor(Rstack, Rp)
+                Q2, R = ops.merge(Rstack)
+                Q = ops.qform(Q2[rank * d:(rank + 1) * d].contiguous())
+            else:
+                R = Rp
+                Q = ops.qform(None)
+            Cm = ops.qt(Q, A_loc)
+            if world > 1:
+                dist.all_reduce(Cm)
+            Z, k = ops.trsolve(R, Cm)
+            ops.omega_apply(Z)
+            ev[2 * s + 1].record(stream)
+        barrier()
+    launches = (ks.lib().ks_launch_count() - launches0) if launches0 is not None else None
+    step_ms = [ev[2 * s].elapsed_time(ev[2 * s + 1]) for s in range(args.steps)]
+    sk_ms = [sk_ev[2 * s].elapsed_time(sk_ev[2 * s + 1]) for s in range(args.steps)]
+    t_step = statistics.mean(step_ms)
+    t_sk = statistics.mean(sk_ms)
+    if world > 1:
+        tt = torch.tensor([t_step, t_sk], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_sk = tt.tolist()
+
+    # phase breakdown (one extra, untimed-for-value step)
+    ph = {}
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    flush.fill_(1)
+    e[0].record(stream); Y = ops.sketch(pts); e[1].record(stream)
+    Rp = ops.local_r(Y)
+    if world > 1:
+        Rstack = torch.empty((world * d, d), dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(Rstack, Rp)
+        Q2, R = ops.merge(Rstack)
+        Q = ops.qform(Q2[rank * d:(rank + 1) * d].contiguous())
+    else:
+        R = Rp
+        Q = ops.qform(None)
+    e[2].record(stream)
+    Cm = ops.qt(Q, A_loc)
+    if world > 1:
+        dist.all_reduce(Cm)
+    Z, k = ops.trsolve(R, Cm)
+    ops.omega_apply(Z)
+    e[3].record(stream)
+    torch.cuda.synchronize(dev)
+    ph = {"sketch": e[0].elapsed_time(e[1]), "tsqr_qform": e[1].elapsed_time(e[2]), "solve": e[2].elapsed_time(e[3])}
+
+    # end-to-end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pts_h = torch.as_tensor(pts_np).pin_memory()
+        A_h = torch.as_tensor(np.ascontiguousarray(A_np[rb:re])).pin_memory()
+        X_h = torch.empty((re - rb, m), dtype=torch.float32).pin_memory()
+        pts_d = torch.empty_like(pts)
+        A_d = torch.empty_like(A_loc)
+        tms = []
+        for s in range(args.steps + 1):
+            flush.fill_(s & 0xFF)
+            barrier()
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pts_d.copy_(pts_h, non_blocking=True)
+            A_d.copy_(A_h, non_blocking=True)
+            X, Z, k, R = ksd.lowrank_solve_sharded(ops, pts_d, A_d)
+            X_h.copy_(X, non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            if s > 0:
+                tms.append(a.elapsed_time(b))
+        te = statistics.mean(tms)
+        if world > 1:
+            tt = torch.tensor([te], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = tt.item()
+        e2e = {"value": n * n * d / (te * 1e-3), "unit": "n^2*d/s", "ms_per_step": te,
+               "h2d_bytes_per_step": int(pts_h.numel() * 4 + A_h.numel() * 4),
+               "d2h_bytes_per_step": int(X_h.numel() * 4)}
+
+    if rank == 0:
+        peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+        sm_max = float(peaks.get("sm_max_mhz", FALLBACK_SM_MHZ))
+        rows_per_gpu = re - rb
+        units = rows_per_gpu * n  # K elements per sketch launch on this rank
+        if cfg["omega"] == ks_inputs.OMEGA_SRHT:
+            ops_elem = alu_ops_per_element(cfg)
+            achieved = units * ops_elem / (t_sk * 1e-3) / 1e12
+            peak = 148 * 128 * sm_max * 1e6 / 1e12
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "k_sketch_srht", "ops_per_element": ops_elem,
+                    "peak_basis": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
+        else:
+            flops = 2.0 * units * d * 2  # hi/lo split: 2 MMAs per element (split counted)
+            achieved = flops / (t_sk * 1e-3) / 1e12
+            peak = float(peaks.get("bf16_tflops", 1590.0))
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None, "kernel": "k_sketch_gauss",
+                    "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst); fp16 dense = bf16 rate"}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rate, rows, dt, threads = oracle_sample(cfg, pts_np, args.cpu_rows)
+            cpu = {"value": rate, "unit": "n^2*d/s", "cores": threads, "kind": "oracle",
+                   "sample": f"oracle tier-B sketch (fp64 C) of {rows} evenly spaced rows of {args.config} "
+                             f"in {dt:.1f} s; TSQR/solve not in the sample"}
+        out = {
+            "metric": "K Omega sketch throughput (n^2 d/s), end-to-end TSQR low-rank solve",
+            "value": n * n * d / (t_step * 1e-3), "unit": "n^2*d/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (ks_inputs, Philox seeded)",
+            "config": {"workload": args.config, "n": n, "d": d, "dim": cfg["dim"],
+                       "kernel": "sqexp" if cfg["kernel"] == 0 else "matern32",
+                       "omega": "srht" if cfg["omega"] == 0 else "gauss", "blocks_per_gpu": blocks, "m": m,
+                       "parallelism": f"rows x{world}", "l2": "flushed (256 MiB write) between timed steps"},
+            "sketch_n2d_per_s": n * rows_per_gpu * d * world / (t_sk * 1e-3),
+            "sketch_ms": t_sk, "solve_ms": t_step, "phase_ms": ph,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": launches, "k": int(k.item()),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    cfg = dict(ks_inputs.CONFIGS[args.config])
+    cfg["seed"] = ks_inputs.config_seed(args.config)
+    pts = ks_inputs.points(cfg["seed"], cfg["n"], cfg["dim"], cfg["dist"])
+    if args.impl == "reference":
+        run_reference(args, cfg, pts)
+        return
+    A = ks_inputs.rhs(cfg["seed"], cfg["n"], cfg["m"])
+    run_ours(args, cfg, pts, A)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,192 @@
+/*
+ * ks.h -- C-ABI of the B200-native hot path of arXiv 1312.1869
+ * ("blocked approximate inversion of large, nearly rank-deficient covariance
+ * matrices"):
+ *
+ *     sketch       Y = K Omega            K generated on the fly, never stored
+ *     tsqr         Y = Q R                blocked tall-skinny Householder QR
+ *     lowrank      X = Omega R^{-1} Q^T A (truncated; K X = Q Q^T A)
+ *
+ * Citations are PAPER.md line numbers (the paper's LaTeX source); the readings
+ * of silent or garbled passages (L1..L20) are listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer argument named *_dev / documented "device" is a CUDA device
+ *    pointer on the current device; the caller owns all memory (inputs,
+ *    outputs and workspaces).  The library never allocates or frees device
+ *    memory and never frees caller buffers.
+ *  - Matrices are row-major fp32, 16-byte aligned base pointers.
+ *  - Every call is stream-ordered on `stream` and returns after enqueueing
+ *    (no host synchronisation), except where documented (ks_trsolve tau == 0).
+ *  - Errors: a ks_status is returned; ks_last_error() gives a thread-local
+ *    message.  Invalid arguments are detected before anything is enqueued.
+ *    No C++ exception crosses this boundary.
+ *  - Determinism: Y is bitwise reproducible for given (inputs, seed) and its
+ *    rows do not depend on the row range requested (multi-GPU sharding).
+ *    R/Q are reproducible for fixed (rows, d, blocks).
+ */
+#ifndef KS_H_
+#define KS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define KS_API __attribute__((visibility("default")))
+#else
+#define KS_API
+#endif
+
+typedef struct CUstream_st* ks_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum ks_status {
+  KS_OK = 0,
+  KS_ERR_INVALID_ARGUMENT = 1, /* any precondition violation */
+  KS_ERR_SINGULAR = 2,         /* ks_trsolve, tau == 0: |r_jj| <= 1e-12 max|r_ii| */
+  KS_ERR_CUDA = 3,             /* a CUDA runtime / driver call failed */
+  KS_ERR_OOM = 4,              /* workspace smaller than the *_workspace_size answer */
+  KS_ERR_UNSUPPORTED = 5,      /* valid request outside what the kernels implement */
+  KS_ERR_NCCL = 6              /* reserved: collectives run in the Python layer */
+} ks_status;
+
+/* Covariance kernels (configs).  r^2 = sum_c (x_c - y_c)^2
+ * by direct differences (reading L10).
+ *   KS_KERNEL_SQEXP    k = sigma2 * exp(-r^2 / (2 ell^2))               (L7)
+ *   KS_KERNEL_MATERN32 k = sigma2 * (1 + sqrt3 r/ell) exp(-sqrt3 r/ell) (L8) */
+typedef enum ks_kernel_kind { KS_KERNEL_SQEXP = 0, KS_KERNEL_MATERN32 = 1 } ks_kernel_kind;
+
+/* Random projection Omega (n x d):
+ *   KS_OMEGA_SRHT  Def. 1, T = Walsh-Hadamard (:74-89):
+ *                  Omega = D_s H_N[:, S] / sqrt(N), natural order, N = 2^ceil(log2 n),
+ *                  K zero-padded to N columns (readings L1-L4).
+ *   KS_OMEGA_GAUSS PAPER.md:54: Omega_ij = fp16_RN(z_ij) / sqrt(d), z ~ N(0,1) (L6). */
+typedef enum ks_omega_kind { KS_OMEGA_SRHT = 0, KS_OMEGA_GAUSS = 1 } ks_omega_kind;
+
+typedef struct ks_sketch_desc {
+  int64_t n;       /* number of points = order of K, n >= 1 */
+  int32_t dim;     /* point dimension, 1..3 */
+  int32_t kernel;  /* ks_kernel_kind */
+  float sigma2;    /* > 0 */
+  float ell;       /* > 0 */
+  float nugget;    /* >= 0, added to K's diagonal by index (L9) */
+  int32_t d;       /* sketch width, 1 <= d <= N; SRHT: d <= 512; GAUSS: d % 16 == 0, 16 <= d <= 256 */
+  uint64_t seed;   /* Philox4x32-10 key */
+  int32_t omega;   /* ks_omega_kind */
+  int32_t reserved;
+} ks_sketch_desc;
+
+/* ------------------------------------------------------------------ sketch */
+
+/* Device workspace bytes needed by ks_sketch / ks_omega_apply / ks_omega_export. */
+KS_API ks_status ks_sketch_workspace_size(const ks_sketch_desc* desc, size_t* bytes);
+
+/* Y = rows [row_begin, row_end) of K Omega  (PAPER.md:95 "K-hat = K Omega", :19).
+ *   pts_dev : device, fp32 SoA, dim x n (coordinate c of point j at pts[c*n + j])
+ *   Y_dev   : device, fp32, (row_end - row_begin) x d, row-major
+ *   ws_dev  : device workspace of ks_sketch_workspace_size bytes (contents
+ *             after the call: the sketch randomness, reused by ks_omega_apply)
+ * Generates the randomness (signs, selection, Gaussian Omega) in the workspace,
+ * then runs the fused covariance-tile + transform kernel.  K is never stored.
+ * Errors: INVALID_ARGUMENT (desc out of range, 0 <= row_begin <= row_end <= n
+ * violated, null pointers), OOM (ws_bytes too small), UNSUPPORTED (d above the
+ * kernel limits), CUDA. */
+KS_API ks_status ks_sketch(const ks_sketch_desc* desc, const float* pts_dev, int64_t row_begin, int64_t row_end,
+                    float* Y_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+
+/* Export the sketch randomness for bit-exact tests (device outputs; any may be NULL):
+ *   signs_dev  int8[N]       s_j in {-1,+1}      (Def. 1 "Rademacher")
+ *   sel_dev    int32[d]      S sorted ascending  (Def. 1 "permutation submatrix", :70)
+ *   gauss_dev  uint16[n*d]   fp16 bits of Omega_ij * sqrt(d), row-major n x d (GAUSS only) */
+KS_API ks_status ks_omega_export(const ks_sketch_desc* desc, int8_t* signs_dev, int32_t* sel_dev, uint16_t* gauss_dev,
+                          void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+
+/* X = rows [row_begin, row_end) of Omega Z  (reading L14: K X = Y Z).
+ *   Z_dev : device, d x m fp32;  X_dev : device, (row_end-row_begin) x m fp32.
+ *   1 <= m <= 64.  Regenerates the randomness into ws_dev (same size as ks_sketch). */
+KS_API ks_status ks_omega_apply(const ks_sketch_desc* desc, const float* Z_dev, int32_t m, int64_t row_begin,
+                         int64_t row_end, float* X_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+
+/* -------------------------------------------------------------------- TSQR */
+
+/* Blocked TSQR, eqs. (1)-(4): the rows are split into `blocks`
+ * contiguous, equal-as-possible blocks (L13); each block is factored by
+ * Householder QR (internally as a binary sub-tree of row leaves of <= 1024
+ * rows -- "any Householder-based scheme", R is unique); stacked R's are merged
+ * pairwise, an odd one passing through.  R is upper triangular with exact
+ * zeros below the diagonal and r_jj >= 0 (L12).
+ * Limits: 1 <= d <= 512, every block must have >= d rows. */
+typedef struct ks_tsqr_plan* ks_tsqr_handle;
+
+KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks, size_t* bytes);
+
+/* Create a plan over a caller-owned device workspace (kept until destroy). */
+KS_API ks_status ks_tsqr_create(int64_t rows, int32_t d, int32_t blocks, void* ws_dev, size_t ws_bytes,
+                         ks_tsqr_handle* out);
+KS_API ks_status ks_tsqr_destroy(ks_tsqr_handle h);
+
+/* Factor Y (device, rows x d, not modified).  R_dev: d x d output.  If Q_dev is
+ * non-NULL the explicit Q (rows x d, Q^T Q = I) is formed: Q-hat = Q^b_1 Q^b_2 ...
+ * (eq. 4).  The implicit factors stay in the handle for ks_qform. */
+KS_API ks_status ks_tsqr(ks_tsqr_handle h, const float* Y_dev, float* Q_dev, float* R_dev, ks_stream_t stream);
+
+/* Q_dev (rows x d) = Q-hat * C, with C (d x d, device) or C = I if C_dev == NULL.
+ * Multi-GPU second level: C = this rank's d x d block of the merge's Q2. */
+KS_API ks_status ks_qform(ks_tsqr_handle h, const float* C_dev, float* Q_dev, ks_stream_t stream);
+
+/* Second TSQR level (eq. (5)'s final merge of per-unit R's):
+ * QR of the stacked (P*d) x d matrix of per-rank R's.  Q2_dev: (P*d) x d
+ * explicit, R_dev: d x d.  Run redundantly on every rank. */
+KS_API ks_status ks_tsqr_merge_workspace_size(int32_t P, int32_t d, size_t* bytes);
+KS_API ks_status ks_tsqr_merge(const float* Rstack_dev, int32_t P, int32_t d, float* Q2_dev, float* R_dev, void* ws_dev,
+                        size_t ws_bytes, ks_stream_t stream);
+
+/* ------------------------------------------------------------------- solve */
+
+/* C = Q^T X (explicit Q, "Q-hat^T x ... evaluated via blocking").
+ *   Q_dev rows x d, X_dev rows x m, C_dev d x m (1 <= m <= 64).  Deterministic
+ *   two-stage reduction over row chunks (no atomics). */
+KS_API ks_status ks_apply_qt_workspace_size(int64_t rows, int32_t d, int32_t m, size_t* bytes);
+KS_API ks_status ks_apply_qt(const float* Q_dev, int64_t rows, int32_t d, const float* X_dev, int32_t m, float* C_dev,
+                      void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+
+/* X = Q C (explicit Q; rows x d times d x m). */
+KS_API ks_status ks_apply_q(const float* Q_dev, int64_t rows, int32_t d, const float* C_dev, int32_t m, float* X_dev,
+                     ks_stream_t stream);
+
+/* Truncated back substitution ("R^{-1} ... by backward substitution";
+ * upper triangular per :95, reading L11; truncation L14):
+ *   tau > 0 : k = largest prefix with |r_jj| >= tau * max_i |r_ii|;
+ *             Z[:k] = R[:k,:k]^{-1} C[:k], Z[k:] = 0; *k_dev = k.  Async.
+ *   tau == 0: strict; if any |r_jj| <= 1e-12 max|r_ii| returns KS_ERR_SINGULAR
+ *             (message names the index).  Synchronises `stream`.
+ *   R_dev d x d, C_dev/Z_dev d x m (device fp32); computed in fp64 on the GPU.
+ *   k_dev: device int32 (may be NULL). */
+KS_API ks_status ks_trsolve(const float* R_dev, const float* C_dev, int32_t d, int32_t m, float tau, float* Z_dev,
+                     int32_t* k_dev, ks_stream_t stream);
+
+/* One-shot single-GPU path: sketch -> tsqr -> apply_qt -> trsolve -> omega_apply.
+ *   A_dev n x m, X_dev n x m, Z_dev d x m, k_dev int32 (device).  Workspace
+ *   size from ks_lowrank_workspace_size. */
+KS_API ks_status ks_lowrank_workspace_size(const ks_sketch_desc* desc, int32_t m, int32_t blocks, size_t* bytes);
+KS_API ks_status ks_lowrank_solve(const ks_sketch_desc* desc, const float* pts_dev, const float* A_dev, int32_t m,
+                           int32_t blocks, float tau, float* X_dev, float* Z_dev, int32_t* k_dev, void* ws_dev,
+                           size_t ws_bytes, ks_stream_t stream);
+
+/* Thread-local description of the last error ("" if none). */
+KS_API const char* ks_last_error(void);
+
+/* Library version string. */
+KS_API const char* ks_version(void);
+
+/* Number of kernels this library has enqueued since load (process-wide,
+ * monotonically increasing; used by bench.py for its gpu_launches claim). */
+KS_API uint64_t ks_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_H_ */

@@ -1,0 +1,304 @@
+// ks_gauss.cu -- Gaussian-Omega sketch on the 5th-generation tensor cores (sm_100a).
+//
+//   Y = K Omega,  Omega_jt = fp16(z_jt) / sqrt(d)       (reading L6)
+//
+// "The product B Omega involves O(n^2 d) flops": a true dense
+// contraction, so it runs on tcgen05.  K is never stored: producer warps
+// evaluate a 128 x 64 tile of K in registers, split it K = K_hi + 2^-11 K_lo'
+// (both fp16, K_lo' = (K - K_hi) * 2^11) and write both halves into shared
+// memory in the UMMA K-major SWIZZLE_128B layout.  Omega^T tiles (d x 64 fp16)
+// arrive by TMA.  One elected thread issues
+//     acc_hi += K_hi Omega ,  acc_lo += K_lo' Omega      (M=128, N=d, K=16 per MMA)
+// with both accumulators in TMEM (2d columns); the epilogue reads them back with
+// tcgen05.ld and writes Y = (acc_hi + 2^-11 acc_lo) / sqrt(d).  Omega's fp16
+// values are exact tensor-core operands, so the only rounding beyond fp32
+// accumulation is the ~2^-22 relative split error of K.
+//
+// Warp roles (384 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
+// allocator + MMA issuer (one lane), warps 4..11 = K-tile producers, then the
+// epilogue.  3-stage mbarrier ring (full: 8 producer warps + TMA tx; empty:
+// tcgen05.commit).
+#include "ks_common.cuh"
+#include "ks_internal.h"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <mutex>
+
+namespace ks {
+
+constexpr int kGStages = 3;
+constexpr int kGThreads = 384;
+constexpr int kATileBytes = kGaussBM * kGaussBK * 2;  // 16 KB per fp16 half
+
+// ----------------------------------------------------------------- PTX helpers
+KS_DEVINL void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+KS_DEVINL void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+KS_DEVINL void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+KS_DEVINL void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+KS_DEVINL void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+KS_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+KS_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+KS_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B (SBO), LBO = 16 B (unused),
+// version 1 (sm_100), base offset 0 (tiles are 1024-aligned).
+KS_DEVINL uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+KS_DEVINL void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+KS_DEVINL void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+KS_DEVINL void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+KS_DEVINL uint32_t pack_half2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// ------------------------------------------------------------------ kernel
+template <int DIM, int KIND>
+__global__ void __launch_bounds__(kGThreads, 1)
+k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict__ pk, int64_t row_begin,
+               int64_t row_end, int nkb, int DN, float nugget, float out_scale, float* __restrict__ Y) {
+  const int kBTileBytes = DN * kGaussBK * 2;
+  const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* a_hi = smem;
+  uint8_t* a_lo = smem + kGStages * kATileBytes;
+  uint8_t* b_t = a_lo + kGStages * kATileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_t + kGStages * kBTileBytes);  // full[S], empty[S], accf
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kGStages + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = row_begin + (int64_t)blockIdx.x * kGaussBM;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kGStages), accf = smem_u32(bars + 2 * kGStages);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kGStages; ++s) {
+      mbar_init(full0 + 8 * s, 8 + 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer: Omega^T tiles (DN x 64)
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kGStages;
+        const uint32_t ph = (kb / kGStages) & 1;
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        mbar_arrive_tx(full0 + 8 * s, kBTileBytes);
+        tma_load_2d(smem_u32(b_t + s * kBTileBytes), &tmB, kb * kGaussBK, 0, full0 + 8 * s);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      // kind::f16 instruction descriptor: D=f32 (bit 4), A=B=f16, both K-major, N>>3 at 17, M>>4 at 24.
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(DN >> 3) << 17) | ((uint32_t)(kGaussBM >> 4) << 24);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kGStages;
+        const uint32_t ph = (kb / kGStages) & 1;
+        mbar_wait(full0 + 8 * s, ph);
+        tc_fence_after();
+        const uint64_t dh = umma_desc_sw128(smem_u32(a_hi + s * kATileBytes));
+        const uint64_t dl = umma_desc_sw128(smem_u32(a_lo + s * kATileBytes));
+        const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBTileBytes));
+#pragma unroll
+        for (int kk = 0; kk < kGaussBK / 16; ++kk) {
+          const uint32_t acc = (kb | kk) != 0;
+          umma_f16(tmem, dh + 2 * kk, db + 2 * kk, idesc, acc);        // +32 B per K=16 step
+          umma_f16(tmem + DN, dl + 2 * kk, db + 2 * kk, idesc, acc);
+        }
+        umma_commit(empty0 + 8 * s);
+      }
+      umma_commit(accf);
+    }
+  } else if (warp >= 4) {
+    // ---------------- K-tile producers: thread p -> rows 4rq..4rq+3, columns 8cq..8cq+7 of the tile
+    const int p = threadIdx.x - 128;
+    const int rq = p >> 3, cq = p & 7;
+    float xi[4][3];
+    int64_t irow[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      int64_t i = row0 + 4 * rq + rr;
+      irow[rr] = i;
+      if (i >= row_end) i = row_end - 1;
+      const float4 q = pk[i];
+      xi[rr][0] = q.x; xi[rr][1] = q.y; xi[rr][2] = q.z;
+    }
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kGStages;
+      const uint32_t ph = (kb / kGStages) & 1;
+      const int64_t j0 = (int64_t)kb * kGaussBK + 8 * cq;
+      float4 pts[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pts[q] = __ldg(pk + j0 + q);
+      mbar_wait(empty0 + 8 * s, ph ^ 1);
+      const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = cov_signed<DIM, KIND>(xi[rr], pts[q]);
+        if (diag) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (j0 + q == irow[rr]) v[q] += nugget;   // nugget by index (reading L9)
+        }
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hi[q] = pack_half2(v[2 * q], v[2 * q + 1]);
+          const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi[q]));
+          lo[q] = pack_half2((v[2 * q] - hf.x) * 2048.0f, (v[2 * q + 1] - hf.y) * 2048.0f);
+        }
+        const int r = 4 * rq + rr;
+        const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(a_hi + s * kATileBytes + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(a_lo + s * kATileBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full0 + 8 * s);
+    }
+    // ---------------- epilogue: TMEM -> registers -> Y
+    mbar_wait(accf, 0);
+    tc_fence_after();
+    const int quarter = warp & 3;             // TMEM lanes 32*quarter .. +31
+    const int half = (warp - 4) >> 2;         // column half
+    const int row = 32 * quarter + lane;
+    const int64_t i = row0 + row;
+    const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
+    for (int c0 = half * (DN / 2); c0 < (half + 1) * (DN / 2); c0 += 8) {
+      float h[8], l[8];
+      tmem_ld8(tl + (uint32_t)c0, h);
+      tmem_ld8(tl + (uint32_t)(DN + c0), l);
+      if (i < row_end) {
+        float4* dst = reinterpret_cast<float4*>(Y + (i - row_begin) * (int64_t)DN + c0);
+        dst[0] = make_float4(fmaf(l[0], 0x1p-11f, h[0]) * out_scale, fmaf(l[1], 0x1p-11f, h[1]) * out_scale,
+                             fmaf(l[2], 0x1p-11f, h[2]) * out_scale, fmaf(l[3], 0x1p-11f, h[3]) * out_scale);
+        dst[1] = make_float4(fmaf(l[4], 0x1p-11f, h[4]) * out_scale, fmaf(l[5], 0x1p-11f, h[5]) * out_scale,
+                             fmaf(l[6], 0x1p-11f, h[6]) * out_scale, fmaf(l[7], 0x1p-11f, h[7]) * out_scale);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+template <int DIM, int KIND>
+static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
+                              char* ws, cudaStream_t st) {
+  auto encode = get_encode();
+  if (!encode) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int DN = D.d;
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)L.ncols_pad, (cuuint64_t)DN};
+  cuuint64_t strides[1] = {(cuuint64_t)L.ncols_pad * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kGaussBK, (cuuint32_t)DN};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ws + L.off_gauss, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  const int smem = 1024 + kGStages * (2 * kATileBytes + DN * kGaussBK * 2) + 256;
+  auto kern = k_sketch_gauss<DIM, KIND>;
+  KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const unsigned grid = (unsigned)((re - rb + kGaussBM - 1) / kGaussBM);
+  const int nkb = (int)(L.ncols_pad / kGaussBK);
+  kern<<<grid, kGThreads, smem, st>>>(tm, reinterpret_cast<const float4*>(ws + L.off_pk), rb, re, nkb, DN, D.nugget,
+                                      (float)(1.0 / std::sqrt((double)D.d)), Y);
+  KS_LAUNCH_CHECK();
+  return KS_OK;
+}
+
+ks_status gauss_sketch_run(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
+                           char* ws, cudaStream_t st) {
+  const bool se = D.kernel == KS_KERNEL_SQEXP;
+  switch (D.dim) {
+    case 1: return se ? launch_gauss<1, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
+                      : launch_gauss<1, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
+    case 2: return se ? launch_gauss<2, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
+                      : launch_gauss<2, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
+    case 3: return se ? launch_gauss<3, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
+                      : launch_gauss<3, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
+  }
+  return fail(KS_ERR_INVALID_ARGUMENT, "dim");
+}
+
+}  // namespace ks

@@ -1,0 +1,75 @@
+// ks_internal.h -- host-side internals shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/ks.h"
+
+namespace ks {
+
+void set_error(const std::string& msg);
+
+// Status helper: records a message and returns the code.
+inline ks_status fail(ks_status code, const std::string& msg) { set_error(msg); return code; }
+
+#define KS_CUDA_TRY(expr)                                                                    \
+  do {                                                                                       \
+    cudaError_t e__ = (expr);                                                                \
+    if (e__ != cudaSuccess)                                                                  \
+      return ::ks::fail(KS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__));   \
+  } while (0)
+
+void count_launch();
+
+// After every <<<...>>> launch: count it (ks_launch_count) and check the launch error.
+#define KS_LAUNCH_CHECK()                \
+  do {                                   \
+    ::ks::count_launch();                \
+    KS_CUDA_TRY(cudaGetLastError());     \
+  } while (0)
+
+#define KS_TRY(expr)                     \
+  do {                                   \
+    ks_status s__ = (expr);              \
+    if (s__ != KS_OK) return s__;        \
+  } while (0)
+
+// ---------------------------------------------------------------- sketch side
+constexpr int kSrhtB = 512;         // SRHT chunk length (columns of K per transform block)
+constexpr int kSrhtRows = 32;       // rows of Y per CTA
+constexpr int kGaussBM = 128;       // rows per tcgen05 tile
+constexpr int kGaussBK = 64;        // reduction (j) block per pipeline stage
+
+struct SketchLayout {
+  int64_t N;          // 2^ceil(log2 n)
+  int64_t ncols_pad;  // packed-point count (multiple of the chunk length)
+  int A;              // number of SRHT chunks covering [0, n)
+  int d_pad;          // SRHT: outputs padded to 32 * TPG
+  int tpg;            // SRHT outputs per thread group
+  size_t off_pk, off_tab, off_sel, off_bucket_ofs, off_bucket_idx, off_bitmap, off_gauss, bytes;
+};
+
+ks_status sketch_validate(const ks_sketch_desc* desc);
+SketchLayout sketch_layout(const ks_sketch_desc& desc);
+// Fill the workspace with this desc's randomness (packed points need pts).
+ks_status sketch_prepare(const ks_sketch_desc& desc, const SketchLayout& L, const float* pts, char* ws,
+                         cudaStream_t st, bool need_points);
+ks_status sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, int64_t row_begin, int64_t row_end,
+                     float* Y, char* ws, cudaStream_t st);
+ks_status omega_apply_run(const ks_sketch_desc& desc, const SketchLayout& L, const float* Z, int m,
+                          int64_t row_begin, int64_t row_end, float* X, char* ws, cudaStream_t st);
+ks_status omega_export_run(const ks_sketch_desc& desc, const SketchLayout& L, int8_t* signs, int32_t* sel,
+                           uint16_t* gauss, char* ws, cudaStream_t st);
+ks_status gauss_sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, int64_t row_begin,
+                           int64_t row_end, float* Y, char* ws, cudaStream_t st);
+
+// ---------------------------------------------------------------- solve side
+ks_status apply_qt_ws(int64_t rows, int d, int m, size_t* bytes);
+ks_status apply_qt_run(const float* Q, int64_t rows, int d, const float* X, int m, float* C, void* ws,
+                       cudaStream_t st);
+ks_status apply_q_run(const float* Q, int64_t rows, int d, const float* C, int m, float* X, cudaStream_t st);
+ks_status trsolve_run(const float* R, const float* C, int d, int m, float tau, float* Z, int32_t* k,
+                      cudaStream_t st);
+
+}  // namespace ks

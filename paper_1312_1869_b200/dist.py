@@ -1,0 +1,108 @@
+"""Row-sharded multi-GPU orchestration (one process per GPU, torch.distributed).
+
+Rows of K, Y, Q, A and X shard naturally.  Rank p owns rows
+[n p / P, n (p+1) / P):
+
+    Y_p   = ks_sketch(rows of rank p)                      no communication (K row-independent)
+    R_p   = local TSQR of Y_p  (the config's blocks per rank)
+    Rstk  = all_gather(R_p)                                C1: P x (d x d)       NVLink / NCCL
+    Q2, R = QR(Rstk)  redundantly on every rank            eq. (5)'s final merge
+    Q_p   = Q_p^(1) Q2[p d : (p+1) d]                      ks_qform
+    C     = all_reduce(sum_p Q_p^T A_p)                    C2: d x m
+    Z, k  = truncated back substitution (redundant)
+    X_p   = rows of rank p of Omega Z
+
+The local steps are supplied by an ``ops`` object so that the same
+orchestration runs on the CUDA library (``CudaOps``, the product) and, in the
+CPU gloo tests, on any other implementation of the same seven steps.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
+    return n * rank // world, n * (rank + 1) // world
+
+
+class CudaOps:
+    """The seven local steps through the C-ABI library (device tensors, current stream)."""
+
+    def __init__(self, desc, m, blocks_per_rank, tau, rank, world, device):
+        from . import (Sketch, TsqrPlan, _desc, _ws, ks_apply_qt, ks_apply_qt_workspace_size, ks_omega_apply,
+                       ks_qform, ks_sketch, ks_trsolve, ks_tsqr)
+        self._f = dict(apply_qt=ks_apply_qt, omega_apply=ks_omega_apply, qform=ks_qform, sketch=ks_sketch,
+                       trsolve=ks_trsolve, tsqr=ks_tsqr)
+        self.desc = _desc(desc)
+        self.m, self.tau = int(m), float(tau)
+        self.device = torch.device(device)
+        n, d = self.desc.n, self.desc.d
+        self.rb, self.re = shard_rows(n, world, rank)
+        rows = self.re - self.rb
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.sk = Sketch(self.desc, self.device)
+        self.plan = TsqrPlan(rows, d, blocks_per_rank, self.device)
+        self.mplan = TsqrPlan(world * d, d, world, self.device) if world > 1 else None
+        self.Y = torch.empty((rows, d), **f32)
+        self.Q = torch.empty((rows, d), **f32)
+        self.Rp = torch.empty((d, d), **f32)
+        self.Q2 = torch.empty((world * d, d), **f32)
+        self.R = torch.empty((d, d), **f32)
+        self.C = torch.empty((d, self.m), **f32)
+        self.Z = torch.empty((d, self.m), **f32)
+        self.X = torch.empty((rows, self.m), **f32)
+        self.k = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.qt_ws = _ws(ks_apply_qt_workspace_size(rows, d, self.m), self.device)
+
+    def sketch(self, pts):
+        self._f["sketch"](self.desc, pts, self.rb, self.re, self.Y, self.sk.ws)
+        return self.Y
+
+    def local_r(self, Y):
+        self._f["tsqr"](self.plan.h, Y, None, self.Rp)
+        return self.Rp
+
+    def merge(self, Rstack):
+        self._f["tsqr"](self.mplan.h, Rstack, self.Q2, self.R)
+        return self.Q2, self.R
+
+    def qform(self, Cblk):
+        self._f["qform"](self.plan.h, Cblk, self.Q)
+        return self.Q
+
+    def qt(self, Q, A):
+        self._f["apply_qt"](Q, Q.shape[0], Q.shape[1], A, self.m, self.C, self.qt_ws)
+        return self.C
+
+    def trsolve(self, R, Cm):
+        self._f["trsolve"](R, Cm, R.shape[0], self.m, self.tau, self.Z, self.k)
+        return self.Z, self.k
+
+    def omega_apply(self, Z):
+        self._f["omega_apply"](self.desc, Z, self.m, self.rb, self.re, self.X, self.sk.ws)
+        return self.X
+
+
+def lowrank_solve_sharded(ops, pts, A_local, group=None):
+    """One pass of the row-sharded hot path; returns (X_local, Z, k, R).  With world size 1 the
+    collectives are skipped and the local TSQR is the whole factorisation."""
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    Y = ops.sketch(pts)
+    Rp = ops.local_r(Y)
+    if world > 1:
+        d = Rp.shape[0]
+        Rstack = torch.empty((world * d, d), dtype=Rp.dtype, device=Rp.device)
+        dist.all_gather_into_tensor(Rstack, Rp.contiguous(), group=group)
+        Q2, R = ops.merge(Rstack)
+        Q = ops.qform(Q2[rank * d:(rank + 1) * d].contiguous())
+    else:
+        R = Rp
+        Q = ops.qform(None)
+    Cm = ops.qt(Q, A_local)
+    if world > 1:
+        dist.all_reduce(Cm, op=dist.ReduceOp.SUM, group=group)
+    Z, k = ops.trsolve(R, Cm)
+    X = ops.omega_apply(Z)
+    return X, Z, k, R

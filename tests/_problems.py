@@ -1,0 +1,30 @@
+"""Shared helpers for the GPU parity tests: seeded problems (ks_inputs) + the oracle side."""
+import numpy as np
+
+import ks_inputs
+import oracle
+
+
+def problem(name=None, seed=None, **over):
+    cfg, pts, A = ks_inputs.make_problem(name, seed=seed, **over)
+    prob = oracle.Problem.from_cfg(cfg, pts)
+    return cfg, pts, A, prob
+
+
+def desc_of(cfg):
+    return dict(n=cfg["n"], dim=cfg["dim"], kernel=cfg["kernel"], sigma2=cfg["sigma2"], ell=cfg["ell"],
+                nugget=cfg["nugget"], d=cfg["d"], seed=cfg["seed"], omega=cfg["omega"])
+
+
+def relF(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def align_rows(Rg, Rr):
+    """Row-sign alignment of R (= column signs of Q) where |r_jj| sits at the noise floor (L12)."""
+    Rg = np.array(Rg, np.float64)
+    s = np.sign(np.sum(Rg * Rr, axis=1))
+    s[s == 0] = 1
+    return Rg * s[:, None]

@@ -1,0 +1,287 @@
+"""GPU path (through the C-ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerances (north_star): Y relative Frobenius <= 1e-5; R <= 1e-4 after row-sign alignment;
+X via rho(Z) = ||A - Y_ref Z||_F / ||A||_F within 1e-4 of rho_ref(k_gpu), |k_gpu - k_ref| <= 1
+(SURVEY.md 8(c) L15).  Signs, selection and the fp16 Gaussian Omega bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from _problems import align_rows, desc_of, problem, relF
+
+pytestmark = pytest.mark.gpu
+
+Y_TOL, R_TOL, RHO_TOL = 1e-5, 1e-4, 1e-4
+
+
+def _t(a, cuda, dtype=None):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a), device=cuda, dtype=dtype)
+
+
+def _gpu_sketch(ks, cfg, pts, cuda, rb=0, re=None):
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    Y = sk(_t(pts, cuda), rb, re)
+    return sk, Y.cpu().numpy()
+
+
+# ---------------------------------------------------------------- randomness
+@pytest.mark.parametrize("n,d,omega", [(2048, 64, 0), (3000, 100, 0), (16384, 128, 0), (100, 10, 0), (64, 64, 0),
+                                       (1000, 64, 1), (4096, 256, 1)])
+def test_randomness_bit_exact(ks, cuda, n, d, omega):
+    cfg, pts, A, prob = problem("c1", n=n, d=d, omega=omega, dim=2, seed=1234 + n)
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    s, S, g = sk.export(signs=True, sel=omega == 0, gauss=omega == 1)
+    assert np.array_equal(s.cpu().numpy(), prob.s)
+    if omega == 0:
+        assert np.array_equal(S.cpu().numpy(), prob.S)
+    else:
+        mism = int(np.sum(g.cpu().numpy().view(np.uint16) != prob.om16))
+        assert mism == 0, f"{mism} fp16 Omega mismatches"
+
+
+# ---------------------------------------------------------------- sketch
+SKETCH_CASES = [
+    # name, overrides
+    ("c1", {}),                                                         # full c1: SE, D=1, d=64
+    ("c2", dict(n=3000, d=100)),                                        # Matern, D=2, ragged n / rows / d
+    ("c4", dict(n=1536, d=512, dim=3)),                                 # SE D=3, d = 512 (TPG 16)
+    ("c5", dict(n=2500, d=256)),                                        # Matern, N(0,I) points, d=256
+    ("c1", dict(n=100, d=10)),                                          # N < chunk length
+    ("c1", dict(n=1, d=1)),                                             # degenerate n = 1
+    ("c3", dict(n=4096, d=256)),                                        # Gaussian, tcgen05, d = 256
+    ("c3", dict(n=1000, d=64)),                                         # Gaussian, ragged n and tiles
+    ("c3", dict(n=2048, d=128, kernel=1, ell=0.05)),                    # Gaussian + Matern
+    ("c3", dict(n=777, d=16, dim=1)),                                   # Gaussian, smallest width
+]
+
+
+@pytest.mark.parametrize("name,over", SKETCH_CASES)
+def test_sketch_matches_oracle(ks, cuda, name, over):
+    cfg, pts, A, prob = problem(name, **over)
+    _, Yg = _gpu_sketch(ks, cfg, pts, cuda)
+    Yr = prob.sketch_rows()
+    assert Yg.shape == Yr.shape
+    err = relF(Yg, Yr)
+    assert err <= Y_TOL, err
+
+
+def test_sketch_rows_independent_of_row_range(ks, cuda):
+    cfg, pts, A, prob = problem("c2", n=4000)
+    _, Yfull = _gpu_sketch(ks, cfg, pts, cuda)
+    _, Ypart = _gpu_sketch(ks, cfg, pts, cuda, 37, 1001)
+    assert np.array_equal(Ypart, Yfull[37:1001])               # bit-identical across sharding
+
+
+def test_sketch_identity_K_gives_omega(ks, cuda):
+    """K = I (points 1 apart, ell tiny): Y = Omega exactly in exact arithmetic."""
+    n = 1024
+    pts = np.arange(n, dtype=np.float32)[None, :] * np.float32(1.0)
+    desc = dict(n=n, dim=1, kernel=0, sigma2=1.0, ell=1e-3, nugget=0.0, d=40, seed=5, omega=0)
+    Y = ks.Sketch(desc, cuda)(_t(pts, cuda)).cpu().numpy()
+    prob = oracle.Problem(pts, 0, 1.0, 1e-3, 0.0, 5, 40, 0)
+    assert relF(Y, prob.omega_dense()) <= 1e-6
+
+
+@pytest.mark.parametrize("name,nrows", [("c2", 2048), ("c3", 96), ("c4", 96), ("c5", 48)])
+def test_sketch_full_config_sampled_rows(ks, cuda, name, nrows):
+    """Full BASELINE sizes in the bench launch configuration; oracle on sampled rows."""
+    cfg, pts, A, prob = problem(name)
+    _, Yg = _gpu_sketch(ks, cfg, pts, cuda)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(cfg["n"], size=nrows, replace=False))
+    rows[0], rows[-1] = 0, cfg["n"] - 1
+    Yr = prob.sketch_rows(rows)
+    err = relF(Yg[rows], Yr)
+    assert err <= Y_TOL, err
+
+
+# ---------------------------------------------------------------- TSQR
+TSQR_CASES = [(2048, 64, 4), (16384, 128, 8), (4096, 256, 16), (8192, 512, 8), (3000, 100, 3), (700, 33, 5),
+              (512, 512, 1)]
+
+
+@pytest.mark.parametrize("rows,d,blocks", TSQR_CASES)
+def test_tsqr_random_matrix_matches_oracle(ks, cuda, rows, d, blocks):
+    rng = np.random.default_rng(rows + d)
+    Y = rng.standard_normal((rows, d)).astype(np.float32)
+    plan = ks.TsqrPlan(rows, d, blocks, cuda)
+    Q, R = plan.factor(_t(Y, cuda))
+    Q, R = Q.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
+    _, Rr = oracle.tsqr_tree(Y.astype(np.float64), blocks, want_q=False)
+    assert np.all(np.tril(R, -1) == 0) and np.all(np.diag(R) >= 0)
+    assert relF(R, Rr) <= R_TOL
+    assert np.linalg.norm(Q.T @ Q - np.eye(d)) <= 1e-4 * np.sqrt(d)
+    assert relF(Q @ R, Y) <= 1e-5
+
+
+@pytest.mark.parametrize("name,over", [("c1", {}), ("c2", {}), ("c3", dict(n=8192, blocks=8)), ("c5", dict(n=8192, blocks=2))])
+def test_tsqr_of_sketch_matches_oracle(ks, cuda, name, over):
+    """Ill-conditioned Y (cond up to ~1e8 at c1): R vs the oracle's TSQR of its own Y."""
+    cfg, pts, A, prob = problem(name, **over)
+    Yr = prob.sketch_rows()
+    Y32 = Yr.astype(np.float32)
+    plan = ks.TsqrPlan(cfg["n"], cfg["d"], cfg["blocks"], cuda)
+    Q, R = plan.factor(_t(Y32, cuda))
+    R = R.cpu().numpy().astype(np.float64)
+    _, Rr = oracle.tsqr_tree(Yr, cfg["blocks"], want_q=False)
+    err = relF(align_rows(R, Rr), Rr)
+    assert err <= R_TOL, err
+
+
+def test_tsqr_merge_and_qform(ks, cuda):
+    """Two-level scheme: per-'rank' TSQR, stacked R merge, Q = Q1 Q2_p."""
+    import torch
+    rng = np.random.default_rng(3)
+    P, rows, d = 4, 1024, 64
+    Y = rng.standard_normal((P * rows, d)).astype(np.float32)
+    Rs, plans, Qs = [], [], []
+    for p in range(P):
+        plan = ks.TsqrPlan(rows, d, 2, cuda)
+        _, R = plan.factor(_t(Y[p * rows:(p + 1) * rows], cuda), want_q=False)
+        plans.append(plan)
+        Rs.append(R)
+    Rstack = torch.cat(Rs, 0).contiguous()
+    Q2 = torch.empty((P * d, d), device=cuda)
+    R = torch.empty((d, d), device=cuda)
+    ws = torch.empty(ks.ks_tsqr_merge_workspace_size(P, d), dtype=torch.uint8, device=cuda)
+    ks.ks_tsqr_merge(Rstack, P, d, Q2, R, ws)
+    for p in range(P):
+        Qs.append(plans[p].qform(Q2[p * d:(p + 1) * d].contiguous()))
+    Q = torch.cat(Qs, 0).cpu().numpy().astype(np.float64)
+    R = R.cpu().numpy().astype(np.float64)
+    _, Rr = oracle.householder_qr(Y.astype(np.float64), want_q=False)
+    assert relF(R, Rr) <= R_TOL
+    assert np.linalg.norm(Q.T @ Q - np.eye(d)) <= 1e-4 * np.sqrt(d)
+    assert relF(Q @ R, Y) <= 1e-5
+
+
+def test_tsqr_full_c4_properties(ks, cuda):
+    """c4 at full size (262144 x 512, 8 blocks): QR = Y, Q^T Q = I, R triangular, r_jj >= 0."""
+    import torch
+    cfg, pts, A, prob = problem("c4")
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    Y = sk(_t(pts, cuda))
+    plan = ks.TsqrPlan(cfg["n"], cfg["d"], cfg["blocks"], cuda)
+    Q, R = plan.factor(Y)
+    assert torch.all(torch.tril(R, -1) == 0) and torch.all(torch.diagonal(R) >= 0)
+    Qd, Rd, Yd = Q.double(), R.double(), Y.double()
+    assert (torch.linalg.norm(Qd @ Rd - Yd) / torch.linalg.norm(Yd)).item() <= 1e-5
+    assert torch.linalg.norm(Qd.T @ Qd - torch.eye(cfg["d"], device=cuda, dtype=torch.float64)).item() <= 1e-3
+
+
+# ---------------------------------------------------------------- solve
+def test_trsolve_hand_example_and_singular(ks, cuda):
+    import torch
+    R = _t(np.array([[2.0, 1.0], [0.0, 4.0]], np.float32), cuda)
+    Cm = _t(np.array([[3.0], [8.0]], np.float32), cuda)
+    Z = torch.empty((2, 1), device=cuda)
+    k = torch.zeros(1, dtype=torch.int32, device=cuda)
+    ks.ks_trsolve(R, Cm, 2, 1, 0.0, Z, k)
+    assert np.array_equal(Z.cpu().numpy(), np.array([[0.5], [2.0]], np.float32))
+    Rs = _t(np.array([[2.0, 1.0], [0.0, 0.0]], np.float32), cuda)
+    with pytest.raises(ks.KsError) as e:
+        ks.ks_trsolve(Rs, Cm, 2, 1, 0.0, Z, k)
+    assert e.value.status == 2 and "index 1" in str(e.value)
+
+
+def test_apply_qt_and_apply_q(ks, cuda):
+    import torch
+    rng = np.random.default_rng(8)
+    rows, d, m = 5000, 96, 7
+    Q = rng.standard_normal((rows, d)).astype(np.float32)
+    X = rng.standard_normal((rows, m)).astype(np.float32)
+    Cm = torch.empty((d, m), device=cuda)
+    ws = torch.empty(ks.ks_apply_qt_workspace_size(rows, d, m), dtype=torch.uint8, device=cuda)
+    ks.ks_apply_qt(_t(Q, cuda), rows, d, _t(X, cuda), m, Cm, ws)
+    ref = Q.astype(np.float64).T @ X.astype(np.float64)
+    assert relF(Cm.cpu().numpy(), ref) <= 1e-5
+    Xo = torch.empty((rows, m), device=cuda)
+    ks.ks_apply_q(_t(Q, cuda), rows, d, Cm, m, Xo)
+    assert relF(Xo.cpu().numpy(), Q.astype(np.float64) @ Cm.cpu().numpy().astype(np.float64)) <= 1e-5
+
+
+@pytest.mark.parametrize("omega", [0, 1])
+def test_omega_apply_matches_oracle(ks, cuda, omega):
+    cfg, pts, A, prob = problem("c1", n=3000, d=64, omega=omega, dim=2)
+    Z = np.random.default_rng(1).standard_normal((64, 5)).astype(np.float32)
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    X = sk.omega_apply(_t(Z, cuda)).cpu().numpy()
+    Xr = prob.omega_apply(Z.astype(np.float64))
+    assert relF(X, Xr) <= 1e-5
+    Xp = sk.omega_apply(_t(Z, cuda), 1000, 2100).cpu().numpy()
+    assert np.array_equal(Xp, X[1000:2100])
+
+
+def _solve_parity(ks, cuda, cfg, pts, A, prob, Yref=None):
+    import torch
+    pipe = ks.Pipeline(desc_of(cfg), cfg["m"], cfg["blocks"], tau=oracle.TAU, device=cuda)
+    pipe(_t(pts, cuda), _t(A, cuda))
+    torch.cuda.synchronize()
+    Zg = pipe.Z.cpu().numpy().astype(np.float64)
+    kg = int(pipe.k.item())
+    out = oracle.lowrank_solve(prob, A, cfg["blocks"], Y=Yref)
+    rho_g = oracle.rho_of(out["Y"], Zg, A)
+    rho_r = out["rho"][kg]
+    assert abs(kg - out["k"]) <= 1, (kg, out["k"])
+    assert abs(rho_g - rho_r) <= RHO_TOL, (rho_g, rho_r)
+    return pipe, out, kg
+
+
+@pytest.mark.parametrize("name,over", [("c1", {}), ("c2", {}), ("c3", dict(n=8192, blocks=4)),
+                                       ("c4", dict(n=8192, blocks=4)), ("c5", dict(n=8192, blocks=2))])
+def test_lowrank_solve_matches_oracle(ks, cuda, name, over):
+    cfg, pts, A, prob = problem(name, **over)
+    pipe, out, kg = _solve_parity(ks, cuda, cfg, pts, A, prob)
+    if cfg["n"] <= 16384:
+        # residual on the user-facing X itself: ||A - K X_gpu|| / ||A|| (streamed K, oracle)
+        X = pipe.X.cpu().numpy().astype(np.float64)
+        KX = _K_times(prob, X)
+        rho_x = np.linalg.norm(A - KX) / np.linalg.norm(A)
+        assert abs(rho_x - out["rho"][kg]) <= RHO_TOL
+
+
+def _K_times(prob, X):
+    n = prob.n
+    out = np.zeros_like(X)
+    for r0 in range(0, n, 1024):
+        idx = np.arange(r0, min(n, r0 + 1024))
+        x = prob.pts.astype(np.float64)
+        r2 = ((x[:, idx, None] - x[:, None, :]) ** 2).sum(0)
+        if prob.kind == oracle.SQEXP:
+            Kb = prob.sigma2 * np.exp(-r2 / (2 * prob.ell**2))
+        else:
+            z = np.sqrt(3 * r2) / prob.ell
+            Kb = prob.sigma2 * (1 + z) * np.exp(-z)
+        Kb[np.arange(len(idx)), idx] += prob.nugget
+        out[idx] = Kb @ X
+    return out
+
+
+def test_one_shot_lowrank_solve_abi(ks, cuda):
+    import torch
+    cfg, pts, A, prob = problem("c1")
+    desc = desc_of(cfg)
+    n, d, m = cfg["n"], cfg["d"], cfg["m"]
+    ws = torch.empty(ks.ks_lowrank_workspace_size(desc, m, cfg["blocks"]), dtype=torch.uint8, device=cuda)
+    X = torch.empty((n, m), device=cuda)
+    Z = torch.empty((d, m), device=cuda)
+    k = torch.zeros(1, dtype=torch.int32, device=cuda)
+    ks.ks_lowrank_solve(desc, _t(pts, cuda), _t(A, cuda), m, cfg["blocks"], oracle.TAU, X, Z, k, ws)
+    out = oracle.lowrank_solve(prob, A, cfg["blocks"])
+    kg = int(k.item())
+    assert abs(kg - out["k"]) <= 1
+    assert abs(oracle.rho_of(out["Y"], Z.cpu().numpy().astype(np.float64), A) - out["rho"][kg]) <= RHO_TOL
+
+
+def test_invalid_arguments_rejected_before_launch(ks, cuda):
+    import torch
+    cfg, pts, A, prob = problem("c1")
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    with pytest.raises(ks.KsError) as e:
+        ks.ks_sketch(desc_of(cfg), _t(pts, cuda), 10, 5, torch.empty((1, 64), device=cuda), sk.ws)
+    assert e.value.status == 1
+    with pytest.raises(ks.KsError) as e:
+        ks.ks_sketch(desc_of(cfg), _t(pts, cuda), 0, 10, torch.empty((10, 64), device=cuda), sk.ws[:100])
+    assert e.value.status == 4
