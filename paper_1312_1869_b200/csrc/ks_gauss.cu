@@ -4,20 +4,19 @@
 //
 // "The product B Omega involves O(n^2 d) flops": a true dense
 // contraction, so it runs on tcgen05.  K is never stored: producer warps
-// evaluate a 128 x 64 tile of K in registers, split it K = K_hi + 2^-11 K_lo'
-// (both fp16, K_lo' = (K - K_hi) * 2^11) and write both halves into shared
-// memory in the UMMA K-major SWIZZLE_128B layout.  Omega^T tiles (d x 64 fp16)
-// arrive by TMA.  One elected thread issues
-//     acc_hi += K_hi Omega ,  acc_lo += K_lo' Omega      (M=128, N=d, K=16 per MMA)
-// with both accumulators in TMEM (2d columns); the epilogue reads them back with
-// tcgen05.ld and writes Y = (acc_hi + 2^-11 acc_lo) / sqrt(d).  Omega's fp16
-// values are exact tensor-core operands, so the only rounding beyond fp32
-// accumulation is the ~2^-22 relative split error of K.
+// evaluate a 128 x 64 tile of S*K in registers (S = gauss_scale, a power of two
+// keeping the split in fp16's normal range), split it S*K = K_hi + K_lo (K_hi =
+// S*K truncated to 10 fraction bits, exact in fp16; K_lo = fp16_RN(S*K - K_hi))
+// and write both halves into shared memory in the UMMA K-major SWIZZLE_128B
+// layout.  Omega^T tiles (d x 64 fp16) arrive by TMA.  One elected thread issues
+//     acc += K_hi Omega ;  acc += K_lo Omega        (M=128, N=d, K=16 per MMA)
+// into ONE fp32 TMEM accumulator.  Omega's fp16 values are exact tensor-core
+// operands, so the operand error is the <= 2^-21 relative split error of K.
+// The tensor core's fp32 accumulation is not round-to-nearest (its error grows
+// linearly with the number of MMAs accumulated: tools/gauss_precision.py), so
+// the column loop is cut into segments whose partial sums are drained from TMEM
+// (double buffered) and added to Y in fp32 by dedicated warps.
 //
-// Warp roles (384 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
-// allocator + MMA issuer (one lane), warps 4..11 = K-tile producers, then the
-// epilogue.  3-stage mbarrier ring (full: 8 producer warps + TMA tx; empty:
-// tcgen05.commit).
 #include "ks_common.cuh"
 #include "ks_internal.h"
 
@@ -25,12 +24,14 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 namespace ks {
 
 constexpr int kGStages = 3;
-constexpr int kGThreads = 384;
+constexpr int kGaussSegKb = 16;   // 1024 columns of K per TMEM accumulation segment
+constexpr int kGThreads = 512;
 constexpr int kATileBytes = kGaussBM * kGaussBK * 2;  // 16 KB per fp16 half
 
 // ----------------------------------------------------------------- PTX helpers
@@ -99,11 +100,42 @@ KS_DEVINL uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+KS_DEVINL void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+// fp32 -> (hi, lo) fp16 pair with hi = x truncated to 10 fraction bits (exact in fp16 for the
+// normal range) and lo = fp16_RN(x - hi) (x - hi is exact in fp32): |x - hi - lo| <= 2^-21 |x|.
+KS_DEVINL void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const float ah = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+  const float bh = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
+  hi = pack_half2(ah, bh);
+  lo = pack_half2(a - ah, b - bh);
+}
+
 // ------------------------------------------------------------------ kernel
+// Warp roles (512 threads):
+//   warp 0      TMA producer of Omega^T tiles (one lane)
+//   warp 1      TMEM allocator + MMA issuer (one lane)
+//   warps 4-11  K-tile producers: 128 x 64 tile of S*K per stage, split hi/lo into SW128 smem
+//   warps 12-15 accumulator drainers (warp 12+q owns TMEM lanes 32q..32q+31 = rows of the tile)
+// The column loop is cut into segments of seg_kb stages.  Segment g accumulates
+//   acc[g & 1] = sum_{stages of g} (K_hi + K_lo) Omega        (both MMAs into ONE accumulator)
+// in TMEM (2 x DN columns, double buffered) and the drainers add it to Y in fp32 (round to nearest)
+// while the MMA runs the next segment: the tensor core's own fp32 accumulation only ever spans
+// 8*seg_kb MMAs, which bounds its (non round-to-nearest) accumulation error.
 template <int DIM, int KIND>
 __global__ void __launch_bounds__(kGThreads, 1)
 k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict__ pk, int64_t row_begin,
-               int64_t row_end, int nkb, int DN, float nugget, float out_scale, float* __restrict__ Y) {
+               int64_t row_end, int nkb, int seg_kb, int DN, float nugget, float out_scale, float* __restrict__ Y) {
   const int kBTileBytes = DN * kGaussBK * 2;
   const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
@@ -111,19 +143,24 @@ k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict
   uint8_t* a_hi = smem;
   uint8_t* a_lo = smem + kGStages * kATileBytes;
   uint8_t* b_t = a_lo + kGStages * kATileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b_t + kGStages * kBTileBytes);  // full[S], empty[S], accf
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kGStages + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_t + kGStages * kBTileBytes);  // full[S], empty[S], accf[2], acce[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kGStages + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = row_begin + (int64_t)blockIdx.x * kGaussBM;
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kGStages), accf = smem_u32(bars + 2 * kGStages);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kGStages);
+  const uint32_t accf0 = smem_u32(bars + 2 * kGStages), acce0 = smem_u32(bars + 2 * kGStages + 2);
+  const int nseg = (nkb + seg_kb - 1) / seg_kb;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kGStages; ++s) {
       mbar_init(full0 + 8 * s, 8 + 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
@@ -151,25 +188,31 @@ k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict
     if (lane == 0) {  // ---------------- MMA issuer
       // kind::f16 instruction descriptor: D=f32 (bit 4), A=B=f16, both K-major, N>>3 at 17, M>>4 at 24.
       const uint32_t idesc = (1u << 4) | ((uint32_t)(DN >> 3) << 17) | ((uint32_t)(kGaussBM >> 4) << 24);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kGStages;
-        const uint32_t ph = (kb / kGStages) & 1;
-        mbar_wait(full0 + 8 * s, ph);
+      for (int g = 0; g < nseg; ++g) {
+        const int buf = g & 1;
+        mbar_wait(acce0 + 8 * buf, ((g >> 1) & 1) ^ 1);  // drainers done with this buffer's previous use
         tc_fence_after();
-        const uint64_t dh = umma_desc_sw128(smem_u32(a_hi + s * kATileBytes));
-        const uint64_t dl = umma_desc_sw128(smem_u32(a_lo + s * kATileBytes));
-        const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBTileBytes));
+        const uint32_t dtm = tmem + (uint32_t)(buf * DN);
+        const int kb1 = min(nkb, (g + 1) * seg_kb);
+        for (int kb = g * seg_kb; kb < kb1; ++kb) {
+          const int s = kb % kGStages;
+          const uint32_t ph = (kb / kGStages) & 1;
+          mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint64_t dh = umma_desc_sw128(smem_u32(a_hi + s * kATileBytes));
+          const uint64_t dl = umma_desc_sw128(smem_u32(a_lo + s * kATileBytes));
+          const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBTileBytes));
 #pragma unroll
-        for (int kk = 0; kk < kGaussBK / 16; ++kk) {
-          const uint32_t acc = (kb | kk) != 0;
-          umma_f16(tmem, dh + 2 * kk, db + 2 * kk, idesc, acc);        // +32 B per K=16 step
-          umma_f16(tmem + DN, dl + 2 * kk, db + 2 * kk, idesc, acc);
+          for (int kk = 0; kk < kGaussBK / 16; ++kk) {
+            umma_f16(dtm, dh + 2 * kk, db + 2 * kk, idesc, (kb != g * seg_kb || kk != 0) ? 1u : 0u);
+            umma_f16(dtm, dl + 2 * kk, db + 2 * kk, idesc, 1u);   // +32 B per K=16 step
+          }
+          umma_commit(empty0 + 8 * s);
         }
-        umma_commit(empty0 + 8 * s);
+        umma_commit(accf0 + 8 * buf);
       }
-      umma_commit(accf);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 12) {
     // ---------------- K-tile producers: thread p -> rows 4rq..4rq+3, columns 8cq..8cq+7 of the tile
     const int p = threadIdx.x - 128;
     const int rq = p >> 3, cq = p & 7;
@@ -204,11 +247,7 @@ k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict
         }
         uint32_t hi[4], lo[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          hi[q] = pack_half2(v[2 * q], v[2 * q + 1]);
-          const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi[q]));
-          lo[q] = pack_half2((v[2 * q] - hf.x) * 2048.0f, (v[2 * q + 1] - hf.y) * 2048.0f);
-        }
+        for (int q = 0; q < 4; ++q) split2(v[2 * q], v[2 * q + 1], hi[q], lo[q]);
         const int r = 4 * rq + rr;
         const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
         *reinterpret_cast<uint4*>(a_hi + s * kATileBytes + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
@@ -218,25 +257,39 @@ k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict
       __syncwarp();
       if (lane == 0) mbar_arrive(full0 + 8 * s);
     }
-    // ---------------- epilogue: TMEM -> registers -> Y
-    mbar_wait(accf, 0);
-    tc_fence_after();
-    const int quarter = warp & 3;             // TMEM lanes 32*quarter .. +31
-    const int half = (warp - 4) >> 2;         // column half
+  } else if (warp >= 12) {
+    // ---------------- drainers: Y[row, :] (+)= acc[g & 1][row, :] in fp32, scaled after the last segment
+    const int quarter = warp & 3;
     const int row = 32 * quarter + lane;
     const int64_t i = row0 + row;
+    const bool ok = i < row_end;
+    float* yr = Y + (i - row_begin) * (int64_t)DN;
     const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
-    for (int c0 = half * (DN / 2); c0 < (half + 1) * (DN / 2); c0 += 8) {
-      float h[8], l[8];
-      tmem_ld8(tl + (uint32_t)c0, h);
-      tmem_ld8(tl + (uint32_t)(DN + c0), l);
-      if (i < row_end) {
-        float4* dst = reinterpret_cast<float4*>(Y + (i - row_begin) * (int64_t)DN + c0);
-        dst[0] = make_float4(fmaf(l[0], 0x1p-11f, h[0]) * out_scale, fmaf(l[1], 0x1p-11f, h[1]) * out_scale,
-                             fmaf(l[2], 0x1p-11f, h[2]) * out_scale, fmaf(l[3], 0x1p-11f, h[3]) * out_scale);
-        dst[1] = make_float4(fmaf(l[4], 0x1p-11f, h[4]) * out_scale, fmaf(l[5], 0x1p-11f, h[5]) * out_scale,
-                             fmaf(l[6], 0x1p-11f, h[6]) * out_scale, fmaf(l[7], 0x1p-11f, h[7]) * out_scale);
+    for (int g = 0; g < nseg; ++g) {
+      const int buf = g & 1;
+      mbar_wait(accf0 + 8 * buf, (g >> 1) & 1);
+      tc_fence_after();
+      const bool first = g == 0, last = g == nseg - 1;
+      for (int c0 = 0; c0 < DN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + (uint32_t)(buf * DN + c0), v);
+        if (ok) {
+          float4* dst = reinterpret_cast<float4*>(yr + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float4 a = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            if (!first) {
+              const float4 o = dst[q];
+              a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+            }
+            if (last) { a.x *= out_scale; a.y *= out_scale; a.z *= out_scale; a.w *= out_scale; }
+            dst[q] = a;
+          }
+        }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acce0 + 8 * buf);
     }
   }
   tc_fence_before();
@@ -261,6 +314,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// Stages per accumulation segment (bounds the tensor core's fp32 accumulation
+// run to 8 * seg_kb MMAs).  KS_GAUSS_SEG overrides it for the precision study (tools/gauss_precision.py).
+static int gauss_seg_kb() {
+  static int v = [] {
+    const char* e = getenv("KS_GAUSS_SEG");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? x : kGaussSegKb;
+  }();
+  return v;
+}
+
 template <int DIM, int KIND>
 static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
                               char* ws, cudaStream_t st) {
@@ -281,8 +345,9 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = (unsigned)((re - rb + kGaussBM - 1) / kGaussBM);
   const int nkb = (int)(L.ncols_pad / kGaussBK);
-  kern<<<grid, kGThreads, smem, st>>>(tm, reinterpret_cast<const float4*>(ws + L.off_pk), rb, re, nkb, DN, D.nugget,
-                                      (float)(1.0 / std::sqrt((double)D.d)), Y);
+  const double S = gauss_scale(D);
+  kern<<<grid, kGThreads, smem, st>>>(tm, reinterpret_cast<const float4*>(ws + L.off_pk), rb, re, nkb, gauss_seg_kb(),
+                                      DN, (float)(S * D.nugget), (float)(1.0 / (S * std::sqrt((double)D.d))), Y);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }

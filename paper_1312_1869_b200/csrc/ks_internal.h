@@ -51,6 +51,9 @@ struct SketchLayout {
 };
 
 ks_status sketch_validate(const ks_sketch_desc* desc);
+// Gaussian path: K is generated pre-multiplied by S = 2^floor(log2(2^14 / (sigma2 + nugget))) so that
+// its fp16 hi/lo split stays in fp16's normal range (max S*K = 2^14); Y is divided by S at the end.
+double gauss_scale(const ks_sketch_desc& desc);
 SketchLayout sketch_layout(const ks_sketch_desc& desc);
 // Fill the workspace with this desc's randomness (packed points need pts).
 ks_status sketch_prepare(const ks_sketch_desc& desc, const SketchLayout& L, const float* pts, char* ws,

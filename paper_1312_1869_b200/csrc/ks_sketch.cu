@@ -16,6 +16,7 @@
 #include "ks_common.cuh"
 #include "ks_internal.h"
 
+#include <algorithm>
 #include <cmath>
 
 namespace ks {
@@ -80,7 +81,7 @@ ks_status sketch_validate(const ks_sketch_desc* desc) {
 // ============================================================ randomness kernels
 // Packed point j: (scaled coords, amplitude).  SE: coords * sqrt(log2(e) / (2 ell^2)) so that
 // exp(-r^2/(2 ell^2)) = 2^(-r'^2).  Matern-3/2: coords * sqrt(3)/ell so that r' = sqrt(3) r/ell.
-// amplitude = s_j * sigma2 (SRHT; the Rademacher sign folded in) or sigma2 (Gaussian);
+// amplitude = s_j * sigma2 (SRHT; the Rademacher sign folded in) or S * sigma2 (Gaussian, gauss_scale);
 // padded columns j >= n get amplitude 0 (zero padding, reading L3).
 __global__ void k_pack_points(const float* __restrict__ pts, int64_t n, int dim, int64_t ncols_pad, float scale,
                               float sigma2, uint64_t seed, int srht, float4* __restrict__ pk) {
@@ -200,6 +201,13 @@ __global__ void k_gauss_omega(uint64_t seed, int64_t n, int d, int64_t ncols_pad
   omT[(int64_t)t * ncols_pad + j] = h;
 }
 
+double gauss_scale(const ks_sketch_desc& D) {
+  const double kmax = (double)D.sigma2 + (double)D.nugget;
+  int e = (int)std::floor(std::log2(16384.0 / kmax));
+  e = std::max(-60, std::min(60, e));
+  return std::ldexp(1.0, e);
+}
+
 static float coord_scale(const ks_sketch_desc& D) {
   if (D.kernel == KS_KERNEL_SQEXP) return (float)std::sqrt(1.4426950408889634 / (2.0 * (double)D.ell * (double)D.ell));
   return (float)(std::sqrt(3.0) / (double)D.ell);
@@ -210,7 +218,8 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
   const int srht = D.omega == KS_OMEGA_SRHT;
   if (need_points) {
     const int64_t nb = (L.ncols_pad + 255) / 256;
-    k_pack_points<<<(unsigned)nb, 256, 0, st>>>(pts, D.n, D.dim, L.ncols_pad, coord_scale(D), D.sigma2, D.seed,
+    const float amp = srht ? D.sigma2 : (float)(D.sigma2 * gauss_scale(D));
+    k_pack_points<<<(unsigned)nb, 256, 0, st>>>(pts, D.n, D.dim, L.ncols_pad, coord_scale(D), amp, D.seed,
                                                  srht, reinterpret_cast<float4*>(ws + L.off_pk));
     KS_LAUNCH_CHECK();
   }
