@@ -113,58 +113,92 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+# ------------------------------------------------------------------ shared line fields
+METRIC = "K Omega sketch throughput (n^2 d/s) and end-to-end TSQR low-rank solve time vs n"
+UNIT = "n^2*d/s"
+
+
+def blocks_for(cfg, world):
+    """TSQR leaf blocks per GPU: c4/c5 fix blocks per GPU; the others split the config's blocks."""
+    return cfg["blocks"] if cfg.get("blocks_per_gpu") else max(1, cfg["blocks"] // world)
+
+
+def make_config(name, cfg, world):
+    return {"workload": name, "n": cfg["n"], "d": cfg["d"], "dim": cfg["dim"],
+            "kernel": "sqexp" if cfg["kernel"] == 0 else "matern32",
+            "omega": "srht" if cfg["omega"] == 0 else "gauss", "blocks_per_gpu": blocks_for(cfg, world),
+            "m": cfg["m"], "parallelism": f"rows x{world}",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
 # ------------------------------------------------------------------ oracle leg (cpu_baseline / --impl reference)
-def oracle_sample(cfg, pts, rows_hint=0, budget_s=12.0):
-    """Time the oracle (as it stands) on a bounded row sample of the sketch; returns
-    (n2d_per_s, rows, seconds, threads)."""
-    import oracle
-    prob = oracle.Problem.from_cfg(cfg, pts)
-    _ = prob.s, prob.S  # randomness (excluded, like the GPU's setup)
-    threads = oracle._threads()
-    n, d = cfg["n"], cfg["d"]
-    if rows_hint:
-        rows = rows_hint
-    else:  # calibrate on a small sample, then size it to ~budget_s
-        probe = max(threads, 8)
+class OracleStep:
+    """One oracle 'step' on a bounded sample of the workload (the oracle as it stands, fp64 C,
+    all host threads): the sketch of r evenly spaced rows of Y, the TSQR (explicit Q) and Q^T A of
+    that r x d sample -- all linear in the number of rows, so their time is scaled by n / r --
+    plus the truncated back substitution and the full X = Omega Z once."""
+
+    def __init__(self, cfg, pts, A, budget_s=6.0, rows_hint=0):
+        import oracle
+        self.oracle = oracle
+        self.cfg = cfg
+        self.prob = oracle.Problem.from_cfg(cfg, pts)
+        _ = self.prob.s, self.prob.S  # randomness (setup, excluded like the GPU's)
+        if cfg["omega"] == 1:
+            _ = self.prob.om16
+        self.threads = oracle._threads()
+        n, d = cfg["n"], cfg["d"]
+        if rows_hint:
+            rows = rows_hint
+        else:  # calibrate the sketch on a small sample, then size the sample to ~budget_s
+            probe = max(self.threads, 8)
+            t0 = time.perf_counter()
+            self.prob.sketch_rows(np.arange(probe, dtype=np.int64))
+            dt = time.perf_counter() - t0
+            rows = int(max(probe, min(n, probe * budget_s / max(dt, 1e-3))))
+        self.rows = int(min(n, max(rows, d)))
+        self.sel = np.linspace(0, n - 1, self.rows).astype(np.int64)
+        self.A = np.asarray(A, np.float64)
+        self.sample = (f"oracle (fp64 C, {self.threads} threads): sketch of {self.rows} evenly spaced rows of Y, "
+                       f"TSQR with explicit Q and Q^T A of that {self.rows}x{d} sample, times n/{self.rows}; "
+                       f"truncated back substitution and the full X = Omega Z once")
+
+    def run(self):
+        o, n = self.oracle, self.cfg["n"]
         t0 = time.perf_counter()
-        prob.sketch_rows(np.arange(probe, dtype=np.int64))
-        dt = time.perf_counter() - t0
-        rows = int(max(probe, min(n, probe * budget_s / max(dt, 1e-3))))
-        rows = max(threads, (rows // threads) * threads)
-    sel = np.linspace(0, n - 1, rows).astype(np.int64)
-    t0 = time.perf_counter()
-    prob.sketch_rows(sel)
-    dt = time.perf_counter() - t0
-    return rows * n * d / dt, rows, dt, threads
+        Y = self.prob.sketch_rows(self.sel)
+        Q, R = o.tsqr_tree(Y, max(1, min(self.threads, self.rows // (2 * self.cfg['d']))), want_q=True)
+        Cm = o.matmul(np.ascontiguousarray(Q.T), self.A[self.sel])
+        t_lin = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        k = o.truncation_rank(R)
+        Z = o.back_substitute(R, Cm, k)
+        self.prob.omega_apply(Z)
+        t_once = time.perf_counter() - t1
+        return t_lin * n / self.rows + t_once
+
+    def value(self, seconds):
+        c = self.cfg
+        return c["n"] * c["n"] * c["d"] / seconds
 
 
-def run_reference(args, cfg, pts):
+def run_reference(args, cfg, pts, A):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    rate, rows, dt, threads = oracle_sample(cfg, pts, args.cpu_rows)
-    per_step_rows = rows
-    times = []
-    import oracle
-    prob = oracle.Problem.from_cfg(cfg, pts)
-    sel = np.linspace(0, cfg["n"] - 1, per_step_rows).astype(np.int64)
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state worth amortising
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        prob.sketch_rows(sel)
-        times.append(time.perf_counter() - t0)
-    n, d = cfg["n"], cfg["d"]
-    v = per_step_rows * n * d / statistics.mean(times)
-    sample = f"oracle tier-B sketch (fp64 C, {threads} threads) of {per_step_rows} evenly spaced rows of {args.config}; TSQR/solve not in the sample"
+    st = OracleStep(cfg, pts, A, rows_hint=args.cpu_rows)
+    for _ in range(max(0, min(args.warmup, 1))):
+        st.run()
+    times = [st.run() for _ in range(args.steps)]
+    t = statistics.mean(times)
+    v = st.value(t)
     print(json.dumps({
-        "impl": "reference", "metric": "K Omega sketch throughput (n^2 d/s), end-to-end low-rank solve",
-        "value": v, "unit": "n^2*d/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "n": n, "d": d, "sample_rows": per_step_rows},
-        "cpu_baseline": {"value": v, "unit": "n^2*d/s", "cores": threads, "kind": "oracle", "sample": sample},
-        "e2e": {"value": v, "unit": "n^2*d/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (ks_inputs, Philox seeded)",
+        "config": make_config(args.config, cfg, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": st.threads, "kind": "oracle", "sample": st.sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
@@ -182,9 +216,7 @@ def run_ours(args, cfg, pts_np, A_np):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     n, d, m = cfg["n"], cfg["d"], cfg["m"]
-    blocks = cfg["blocks"]  # per GPU for c4/c5 ("blocks_per_gpu"), else split evenly
-    if not cfg.get("blocks_per_gpu"):
-        blocks = max(1, blocks // world)
+    blocks = blocks_for(cfg, world)
     rb, re = ksd.shard_rows(n, world, rank)
     desc = dict(n=n, dim=cfg["dim"], kernel=cfg["kernel"], sigma2=cfg["sigma2"], ell=cfg["ell"],
                 nugget=cfg["nugget"], d=d, seed=cfg["seed"], omega=cfg["omega"])
@@ -320,19 +352,16 @@ def run_ours(args, cfg, pts_np, A_np):
                     "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst); fp16 dense = bf16 rate"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rate, rows, dt, threads = oracle_sample(cfg, pts_np, args.cpu_rows)
-            cpu = {"value": rate, "unit": "n^2*d/s", "cores": threads, "kind": "oracle",
-                   "sample": f"oracle tier-B sketch (fp64 C) of {rows} evenly spaced rows of {args.config} "
-                             f"in {dt:.1f} s; TSQR/solve not in the sample"}
+            st = OracleStep(cfg, pts_np, A_np, rows_hint=args.cpu_rows)
+            t_or = st.run()
+            cpu = {"value": st.value(t_or), "unit": UNIT, "cores": st.threads, "kind": "oracle",
+                   "sample": st.sample, "extrapolated_s_per_step": t_or}
         out = {
-            "metric": "K Omega sketch throughput (n^2 d/s), end-to-end TSQR low-rank solve",
-            "value": n * n * d / (t_step * 1e-3), "unit": "n^2*d/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC,
+            "value": n * n * d / (t_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (ks_inputs, Philox seeded)",
-            "config": {"workload": args.config, "n": n, "d": d, "dim": cfg["dim"],
-                       "kernel": "sqexp" if cfg["kernel"] == 0 else "matern32",
-                       "omega": "srht" if cfg["omega"] == 0 else "gauss", "blocks_per_gpu": blocks, "m": m,
-                       "parallelism": f"rows x{world}", "l2": "flushed (256 MiB write) between timed steps"},
+            "config": make_config(args.config, cfg, world),
             "sketch_n2d_per_s": n * rows_per_gpu * d * world / (t_sk * 1e-3),
             "sketch_ms": t_sk, "solve_ms": t_step, "phase_ms": ph,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
@@ -349,10 +378,10 @@ def main():
     cfg = dict(ks_inputs.CONFIGS[args.config])
     cfg["seed"] = ks_inputs.config_seed(args.config)
     pts = ks_inputs.points(cfg["seed"], cfg["n"], cfg["dim"], cfg["dist"])
-    if args.impl == "reference":
-        run_reference(args, cfg, pts)
-        return
     A = ks_inputs.rhs(cfg["seed"], cfg["n"], cfg["m"])
+    if args.impl == "reference":
+        run_reference(args, cfg, pts, A)
+        return
     run_ours(args, cfg, pts, A)
 
 

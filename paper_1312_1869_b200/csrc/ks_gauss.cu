@@ -300,6 +300,234 @@ k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict
   }
 }
 
+// ------------------------------------------------------------------ 2-CTA kernel (cta_group::2)
+// A CTA pair (cluster of 2, same TPC) computes a 256-row tile with M = 256 MMAs issued by the leader:
+// each CTA supplies its own 128 rows of K (A operand, produced in its smem) and HALF of Omega^T
+// (B operand, N/2 = d/2 rows by TMA); the accumulator rows live in each CTA's own TMEM.  This halves
+// the shared-memory operand traffic per SM of the 1-CTA kernel (which is smem-bandwidth bound).
+// Barriers: the MMA waits on the LEADER's full[s] (producers of both CTAs arrive remotely; both TMAs
+// complete_tx on it) and acce[b] (drainers of both CTAs arrive); its commits multicast to both CTAs'
+// empty[s] / accf[b].
+constexpr int kG2Stages = 4;
+
+KS_DEVINL uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+KS_DEVINL uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+KS_DEVINL void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+KS_DEVINL void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+KS_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+KS_DEVINL void tma_load_2d_2cta(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+KS_DEVINL void umma_f16_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+KS_DEVINL void umma_commit_2cta(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int DIM, int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGThreads, 1)
+k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restrict__ pk, int64_t row_begin,
+                int64_t row_end, int nkb, int seg_kb, int DN, float nugget, float out_scale, float* __restrict__ Y) {
+  const int kBHalfBytes = (DN / 2) * kGaussBK * 2;
+  const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* a_hi = smem;
+  uint8_t* a_lo = smem + kG2Stages * kATileBytes;
+  uint8_t* b_t = a_lo + kG2Stages * kATileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_t + kG2Stages * kBHalfBytes);  // full[S], empty[S], accf[2], acce[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kG2Stages + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int64_t row0 = row_begin + (int64_t)(blockIdx.x >> 1) * 256 + 128 * (int64_t)rank;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kG2Stages);
+  const uint32_t accf0 = smem_u32(bars + 2 * kG2Stages), acce0 = smem_u32(bars + 2 * kG2Stages + 2);
+  const uint32_t full0_L = mapa_u32(full0, 0), acce0_L = mapa_u32(acce0, 0);   // the leader's barriers
+  const int nseg = (nkb + seg_kb - 1) / seg_kb;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kG2Stages; ++s) {
+      mbar_init(full0 + 8 * s, 16 + 1);   // 8 producer warps x 2 CTAs + the leader's expect_tx
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 8);         // 4 drain warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA: this CTA's half of the Omega^T tile (DN/2 x 64)
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kG2Stages;
+        const uint32_t ph = (kb / kG2Stages) & 1;
+        mbar_wait_cluster(empty0 + 8 * s, ph ^ 1);
+        if (rank == 0) mbar_arrive_tx(full0 + 8 * s, 2 * kBHalfBytes);
+        tma_load_2d_2cta(smem_u32(b_t + s * kBHalfBytes), &tmB, kb * kGaussBK, (int)rank * (DN / 2), full0_L + 8 * s);
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {  // ---------------- MMA issuer (leader only)
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(DN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      for (int g = 0; g < nseg; ++g) {
+        const int buf = g & 1;
+        mbar_wait_cluster(acce0 + 8 * buf, ((g >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + (uint32_t)(buf * DN);
+        const int kb1 = min(nkb, (g + 1) * seg_kb);
+        for (int kb = g * seg_kb; kb < kb1; ++kb) {
+          const int s = kb % kG2Stages;
+          const uint32_t ph = (kb / kG2Stages) & 1;
+          mbar_wait_cluster(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint64_t dh = umma_desc_sw128(smem_u32(a_hi + s * kATileBytes));
+          const uint64_t dl = umma_desc_sw128(smem_u32(a_lo + s * kATileBytes));
+          const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBHalfBytes));
+#pragma unroll
+          for (int kk = 0; kk < kGaussBK / 16; ++kk) {
+            umma_f16_2cta(dtm, dh + 2 * kk, db + 2 * kk, idesc, (kb != g * seg_kb || kk != 0) ? 1u : 0u);
+            umma_f16_2cta(dtm, dl + 2 * kk, db + 2 * kk, idesc, 1u);
+          }
+          umma_commit_2cta(empty0 + 8 * s);
+        }
+        umma_commit_2cta(accf0 + 8 * buf);
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ---------------- K-tile producers: thread p -> rows 4rq..4rq+3, columns 8cq..8cq+7 of the tile
+    const int p = threadIdx.x - 128;
+    const int rq = p >> 3, cq = p & 7;
+    float xi[4][3];
+    int64_t irow[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      int64_t i = row0 + 4 * rq + rr;
+      irow[rr] = i;
+      if (i >= row_end) i = row_end - 1;
+      const float4 q = pk[i];
+      xi[rr][0] = q.x; xi[rr][1] = q.y; xi[rr][2] = q.z;
+    }
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kG2Stages;
+      const uint32_t ph = (kb / kG2Stages) & 1;
+      const int64_t j0 = (int64_t)kb * kGaussBK + 8 * cq;
+      float4 pts[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pts[q] = __ldg(pk + j0 + q);
+      mbar_wait_cluster(empty0 + 8 * s, ph ^ 1);
+      const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = cov_signed<DIM, KIND>(xi[rr], pts[q]);
+        if (diag) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (j0 + q == irow[rr]) v[q] += nugget;   // nugget by index (reading L9)
+        }
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) split2(v[2 * q], v[2 * q + 1], hi[q], lo[q]);
+        const int r = 4 * rq + rr;
+        const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(a_hi + s * kATileBytes + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(a_lo + s * kATileBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(full0_L + 8 * s);
+    }
+  } else if (warp >= 12) {
+    // ---------------- drainers: Y[row, :] (+)= acc[g & 1][row, :] in fp32, scaled after the last segment
+    const int quarter = warp & 3;
+    const int row = 32 * quarter + lane;
+    const int64_t i = row0 + row;
+    const bool ok = i < row_end;
+    float* yr = Y + (i - row_begin) * (int64_t)DN;
+    const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
+    for (int g = 0; g < nseg; ++g) {
+      const int buf = g & 1;
+      mbar_wait_cluster(accf0 + 8 * buf, (g >> 1) & 1);
+      tc_fence_after();
+      const bool first = g == 0, last = g == nseg - 1;
+      for (int c0 = 0; c0 < DN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + (uint32_t)(buf * DN + c0), v);
+        if (ok) {
+          float4* dst = reinterpret_cast<float4*>(yr + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float4 a = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            if (!first) {
+              const float4 o = dst[q];
+              a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+            }
+            if (last) { a.x *= out_scale; a.y *= out_scale; a.z *= out_scale; a.w *= out_scale; }
+            dst[q] = a;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acce0_L + 8 * buf);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -340,14 +568,30 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  const int smem = 1024 + kGStages * (2 * kATileBytes + DN * kGaussBK * 2) + 256;
-  auto kern = k_sketch_gauss<DIM, KIND>;
-  KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const unsigned grid = (unsigned)((re - rb + kGaussBM - 1) / kGaussBM);
+  CUtensorMap tm2;   // half-width boxes (DN/2 rows of Omega^T) for the CTA pair
+  cuuint32_t box2[2] = {(cuuint32_t)kGaussBK, (cuuint32_t)(DN / 2)};
+  r = encode(&tm2, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ws + L.off_gauss, dims, strides, box2, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   const int nkb = (int)(L.ncols_pad / kGaussBK);
   const double S = gauss_scale(D);
-  kern<<<grid, kGThreads, smem, st>>>(tm, reinterpret_cast<const float4*>(ws + L.off_pk), rb, re, nkb, gauss_seg_kb(),
-                                      DN, (float)(S * D.nugget), (float)(1.0 / (S * std::sqrt((double)D.d))), Y);
+  const float nug = (float)(S * D.nugget), osc = (float)(1.0 / (S * std::sqrt((double)D.d)));
+  const float4* pk = reinterpret_cast<const float4*>(ws + L.off_pk);
+  static const bool one_cta = [] { const char* e = getenv("KS_GAUSS_1CTA"); return e && atoi(e) > 0; }();
+  if (one_cta) {
+    const int smem = 1024 + kGStages * (2 * kATileBytes + DN * kGaussBK * 2) + 256;
+    auto kern = k_sketch_gauss<DIM, KIND>;
+    KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const unsigned grid = (unsigned)((re - rb + kGaussBM - 1) / kGaussBM);
+    kern<<<grid, kGThreads, smem, st>>>(tm, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
+  } else {
+    const int smem = 1024 + kG2Stages * (2 * kATileBytes + (DN / 2) * kGaussBK * 2) + 256;
+    auto kern = k_sketch_gauss2<DIM, KIND>;
+    KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const unsigned grid = 2u * (unsigned)((re - rb + 255) / 256);
+    kern<<<grid, kGThreads, smem, st>>>(tm2, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
+  }
   KS_LAUNCH_CHECK();
   return KS_OK;
 }

@@ -37,7 +37,7 @@ void count_launch();
 
 // ---------------------------------------------------------------- sketch side
 constexpr int kSrhtB = 512;         // SRHT chunk length (columns of K per transform block)
-constexpr int kSrhtRows = 32;       // rows of Y per CTA
+constexpr int kSrhtRows = 16;       // rows of Y per CTA
 constexpr int kGaussBM = 128;       // rows per tcgen05 tile
 constexpr int kGaussBK = 64;        // reduction (j) block per pipeline stage
 

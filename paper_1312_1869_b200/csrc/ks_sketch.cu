@@ -241,53 +241,62 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
 }
 
 // ============================================================ fused SRHT kernel
-// One CTA = 32 rows of Y; loops over the column chunks c of K.  256 threads.
-//   phase A : thread (rg = t&7, cg = t>>3) evaluates K*s for rows 4rg..4rg+3, columns
-//             16cg..16cg+15 of the chunk, butterflies over l bits 0-3 in registers,
-//             stores W[l][r] (float4 over 4 rows; conflict-free).
-//   phase B : thread (rp = t&15, lo = t>>4) loads rows 2rp, 2rp+1 at l = lo + 16h, h < 32,
-//             butterflies over l bits 4-8, stores back.  W now holds FWHT_B of the chunk.
-//   phase C : thread (rg = t&7, tg = t>>3) accumulates its TPG outputs for rows 4rg..4rg+3:
-//             acc[k] += (-1)^popc(c & a_t) * W[m_t][4rg .. 4rg+3].
+// One CTA = 16 rows of Y (256 threads, 2+ CTAs per SM); loops over the column chunks c of K.
+// Shared tile W: column l (0..511) of the chunk holds its 16 row values at
+// A(l, r) = l*16 + (l >> 5)*16 + r (the (l >> 5) pad makes phase B conflict-free).
+//   phase A : thread (rg = t&7, cg = t>>3) evaluates K*s for rows 2rg, 2rg+1 and columns
+//             l = cg + 32q, q < 16, butterflies over l bits 5-8 in registers, stores W.
+//   phase B : thread (rp = t&15, g = t>>4) loads row rp at l = 32g + b, b < 32, butterflies
+//             over l bits 0-4, stores back.  W now holds FWHT_B of the chunk (natural order).
+//   phase C : thread (rq = t&3, og = t>>2) accumulates its TPO = TPG/2 outputs for rows
+//             4rq..4rq+3: acc[k] += (-1)^popc(c & a_t) * W[m_t][4rq .. 4rq+3].
+KS_DEVINL int srht_w(int l, int r) { return l * 16 + (l >> 5) * 16 + r; }
+constexpr int kSrhtSmemFloats = kSrhtB * 16 + (kSrhtB / 32) * 16;
+
 template <int DIM, int KIND, int TPG>
-__global__ void __launch_bounds__(256, (TPG <= 4 ? 2 : 1))
+__global__ void __launch_bounds__(256, 2)
 k_sketch_srht(const float4* __restrict__ pk, const uint32_t* __restrict__ tab, int64_t row_begin, int64_t row_end,
               int A, int d, float out_scale, float nugget, float* __restrict__ Y) {
-  extern __shared__ __align__(16) float W[];  // [kSrhtB][32]
+  constexpr int TPO = TPG / 2;
+  __shared__ __align__(16) float W[kSrhtSmemFloats];
   const int t = threadIdx.x;
-  const int rg = t & 7;
-  const int cg = t >> 3;
-  const int rp = t & 15;
-  const int lo = t >> 4;
+  const int rg = t & 7, cg = t >> 3;
+  const int rp = t & 15, g = t >> 4;
+  const int rq = t & 3, og = t >> 2;
   const int64_t row0 = row_begin + (int64_t)blockIdx.x * kSrhtRows;
+  float* wA = W + cg * 16 + 2 * rg;        // + 528 q           (= srht_w(cg + 32 q, 2 rg))
+  float* wB = W + 528 * g + rp;            // + 16 b            (= srht_w(32 g + b, rp))
 
-  float xi[4][3];
+  float xi[2][3];
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    int64_t i = row0 + 4 * rg + rr;
+  for (int rr = 0; rr < 2; ++rr) {
+    int64_t i = row0 + 2 * rg + rr;
     if (i >= row_end) i = row_end - 1;
     const float4 p = pk[i];
     xi[rr][0] = p.x; xi[rr][1] = p.y; xi[rr][2] = p.z;
   }
-  uint32_t tabr[TPG];
+  int wofs[TPO];
+  uint32_t ahi[TPO];
 #pragma unroll
-  for (int k = 0; k < TPG; ++k) tabr[k] = tab[cg * TPG + k];
-  float acc[TPG][4];
+  for (int k = 0; k < TPO; ++k) {
+    const uint32_t e = tab[og * TPO + k];
+    wofs[k] = srht_w((int)(e & 0xFFFFu), 4 * rq);
+    ahi[k] = e >> 16;
+  }
+  float acc[TPO][4];
 #pragma unroll
-  for (int k = 0; k < TPG; ++k)
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) acc[k][rr] = 0.f;
+  for (int k = 0; k < TPO; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.f;
 
   for (int c = 0; c < A; ++c) {
     // ---------------- phase A
     {
-      const float4* pc = pk + (int64_t)c * kSrhtB + 16 * cg;
-      float v[4][16];
+      const float4* pc = pk + (int64_t)c * kSrhtB + cg;
+      float v[2][16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const float4 p = __ldg(pc + q);
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) v[rr][q] = cov_signed<DIM, KIND>(xi[rr], p);
+        const float4 p = __ldg(pc + 32 * q);
+        v[0][q] = cov_signed<DIM, KIND>(xi[0], p);
+        v[1][q] = cov_signed<DIM, KIND>(xi[1], p);
       }
 #pragma unroll
       for (int h = 1; h < 16; h <<= 1)
@@ -295,49 +304,39 @@ k_sketch_srht(const float4* __restrict__ pk, const uint32_t* __restrict__ tab, i
         for (int q = 0; q < 16; ++q)
           if (!(q & h)) {
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-              const float a = v[rr][q], b = v[rr][q + h];
-              v[rr][q] = a + b;
-              v[rr][q + h] = a - b;
+            for (int rr = 0; rr < 2; ++rr) {
+              const float x = v[rr][q], y = v[rr][q + h];
+              v[rr][q] = x + y;
+              v[rr][q + h] = x - y;
             }
           }
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        *reinterpret_cast<float4*>(&W[(16 * cg + q) * 32 + 4 * rg]) = make_float4(v[0][q], v[1][q], v[2][q], v[3][q]);
+      for (int q = 0; q < 16; ++q) *reinterpret_cast<float2*>(wA + 528 * q) = make_float2(v[0][q], v[1][q]);
     }
     __syncthreads();
     // ---------------- phase B
     {
-      float u[2][32];
+      float u[32];
 #pragma unroll
-      for (int h = 0; h < 32; ++h) {
-        const float2 w = *reinterpret_cast<const float2*>(&W[(lo + 16 * h) * 32 + 2 * rp]);
-        u[0][h] = w.x; u[1][h] = w.y;
-      }
+      for (int b = 0; b < 32; ++b) u[b] = wB[16 * b];
 #pragma unroll
-      for (int s = 1; s < 32; s <<= 1)
+      for (int h = 1; h < 32; h <<= 1)
 #pragma unroll
-        for (int h = 0; h < 32; ++h)
-          if (!(h & s)) {
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-              const float a = u[rr][h], b = u[rr][h + s];
-              u[rr][h] = a + b;
-              u[rr][h + s] = a - b;
-            }
+        for (int b = 0; b < 32; ++b)
+          if (!(b & h)) {
+            const float x = u[b], y = u[b + h];
+            u[b] = x + y;
+            u[b + h] = x - y;
           }
 #pragma unroll
-      for (int h = 0; h < 32; ++h)
-        *reinterpret_cast<float2*>(&W[(lo + 16 * h) * 32 + 2 * rp]) = make_float2(u[0][h], u[1][h]);
+      for (int b = 0; b < 32; ++b) wB[16 * b] = u[b];
     }
     __syncthreads();
     // ---------------- phase C
 #pragma unroll
-    for (int k = 0; k < TPG; ++k) {
-      const uint32_t e = tabr[k];
-      const uint32_t m = e & 0xFFFFu, a = e >> 16;
-      const float sg = __int_as_float(0x3f800000u | ((__popc((uint32_t)c & a) & 1u) << 31));
-      const float4 w = *reinterpret_cast<const float4*>(&W[m * 32 + 4 * rg]);
+    for (int k = 0; k < TPO; ++k) {
+      const float sg = __int_as_float(0x3f800000u | ((__popc((uint32_t)c & ahi[k]) & 1u) << 31));
+      const float4 w = *reinterpret_cast<const float4*>(W + wofs[k]);
       acc[k][0] = fmaf(sg, w.x, acc[k][0]);
       acc[k][1] = fmaf(sg, w.y, acc[k][1]);
       acc[k][2] = fmaf(sg, w.z, acc[k][2]);
@@ -348,15 +347,15 @@ k_sketch_srht(const float4* __restrict__ pk, const uint32_t* __restrict__ tab, i
   // ---------------- epilogue: scale, nugget (by index, reading L9), store.
 #pragma unroll
   for (int rr = 0; rr < 4; ++rr) {
-    const int64_t i = row0 + 4 * rg + rr;
+    const int64_t i = row0 + 4 * rq + rr;
     if (i >= row_end) continue;
     const float si = pk[i].w > 0.f ? 1.f : -1.f;
     float* yrow = Y + (i - row_begin) * (int64_t)d;
 #pragma unroll
-    for (int k = 0; k < TPG; ++k) {
-      const int tt = cg * TPG + k;
+    for (int k = 0; k < TPO; ++k) {
+      const int tt = og * TPO + k;
       if (tt < d) {
-        const uint32_t e = tabr[k];
+        const uint32_t e = tab[tt];
         const uint32_t S = (e & 0xFFFFu) + (e >> 16) * (uint32_t)kSrhtB;
         const float h = (__popcll((unsigned long long)i & (unsigned long long)S) & 1) ? -1.f : 1.f;
         yrow[tt] = fmaf(nugget * si, h * out_scale, acc[k][rr] * out_scale);
@@ -369,10 +368,8 @@ template <int DIM, int KIND, int TPG>
 static ks_status launch_srht(const SketchLayout& L, const ks_sketch_desc& D, int64_t rb, int64_t re, float* Y,
                              char* ws, cudaStream_t st) {
   auto kern = k_sketch_srht<DIM, KIND, TPG>;
-  const int smem = kSrhtB * 32 * (int)sizeof(float);
-  KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = (unsigned)((re - rb + kSrhtRows - 1) / kSrhtRows);
-  kern<<<grid, 256, smem, st>>>(reinterpret_cast<const float4*>(ws + L.off_pk),
+  kern<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(ws + L.off_pk),
                                 reinterpret_cast<const uint32_t*>(ws + L.off_tab), rb, re, L.A, D.d,
                                 (float)(1.0 / std::sqrt((double)L.N)), D.nugget, Y);
   KS_LAUNCH_CHECK();
