@@ -498,20 +498,32 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
       mbar_wait_cluster(accf0 + 8 * buf, (g >> 1) & 1);
       tc_fence_after();
       const bool first = g == 0, last = g == nseg - 1;
-      for (int c0 = 0; c0 < DN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tl + (uint32_t)(buf * DN + c0), v);
-        if (ok) {
-          float4* dst = reinterpret_cast<float4*>(yr + c0);
+      for (int c0 = 0; c0 < DN; c0 += 64) {   // 64 columns per batch: all of Y's loads in flight together
+        const int nb = min(64, DN - c0);
+        float4 o[16];
+        if (ok && !first) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float4 a = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            if (!first) {
-              const float4 o = dst[q];
-              a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+          for (int q = 0; q < 16; ++q)
+            if (4 * q < nb) o[q] = reinterpret_cast<const float4*>(yr + c0)[q];
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          if (16 * h < nb) {
+            float v[16];
+            tmem_ld16(tl + (uint32_t)(buf * DN + c0 + 16 * h), v);
+            if (ok) {
+              float4* dst = reinterpret_cast<float4*>(yr + c0 + 16 * h);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                if (!first) {
+                  const float4 y = o[4 * h + q];
+                  x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+                }
+                if (last) { x.x *= out_scale; x.y *= out_scale; x.z *= out_scale; x.w *= out_scale; }
+                dst[q] = x;
+              }
             }
-            if (last) { a.x *= out_scale; a.y *= out_scale; a.z *= out_scale; a.w *= out_scale; }
-            dst[q] = a;
           }
         }
       }

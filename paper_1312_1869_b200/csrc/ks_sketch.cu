@@ -241,7 +241,8 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
 }
 
 // ============================================================ fused SRHT kernel
-// One CTA = 16 rows of Y (256 threads, 2+ CTAs per SM); loops over the column chunks c of K.
+// One CTA = 16 rows of Y (256 threads, 2-3 CTAs per SM); loops over the column chunks c of K.
+// The tile W is double buffered, so a chunk needs 2 barriers (after phase A, after phase B).
 // Shared tile W: column l (0..511) of the chunk holds its 16 row values at
 // A(l, r) = l*16 + (l >> 5)*16 + r (the (l >> 5) pad makes phase B conflict-free).
 //   phase A : thread (rg = t&7, cg = t>>3) evaluates K*s for rows 2rg, 2rg+1 and columns
@@ -251,21 +252,21 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
 //   phase C : thread (rq = t&3, og = t>>2) accumulates its TPO = TPG/2 outputs for rows
 //             4rq..4rq+3: acc[k] += (-1)^popc(c & a_t) * W[m_t][4rq .. 4rq+3].
 KS_DEVINL int srht_w(int l, int r) { return l * 16 + (l >> 5) * 16 + r; }
-constexpr int kSrhtSmemFloats = kSrhtB * 16 + (kSrhtB / 32) * 16;
+constexpr int kSrhtSmemFloats = kSrhtB * 16 + (kSrhtB / 32) * 16;   // 33 KB per buffer
 
 template <int DIM, int KIND, int TPG>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, TPG <= 8 ? 3 : 2)
 k_sketch_srht(const float4* __restrict__ pk, const uint32_t* __restrict__ tab, int64_t row_begin, int64_t row_end,
               int A, int d, float out_scale, float nugget, float* __restrict__ Y) {
   constexpr int TPO = TPG / 2;
-  __shared__ __align__(16) float W[kSrhtSmemFloats];
+  extern __shared__ __align__(16) float Wbuf[];   // [2][kSrhtSmemFloats], double buffered: chunk c uses half c & 1
   const int t = threadIdx.x;
   const int rg = t & 7, cg = t >> 3;
   const int rp = t & 15, g = t >> 4;
   const int rq = t & 3, og = t >> 2;
   const int64_t row0 = row_begin + (int64_t)blockIdx.x * kSrhtRows;
-  float* wA = W + cg * 16 + 2 * rg;        // + 528 q           (= srht_w(cg + 32 q, 2 rg))
-  float* wB = W + 528 * g + rp;            // + 16 b            (= srht_w(32 g + b, rp))
+  const int oA = cg * 16 + 2 * rg;         // + 528 q           (= srht_w(cg + 32 q, 2 rg))
+  const int oB = 528 * g + rp;             // + 16 b            (= srht_w(32 g + b, rp))
 
   float xi[2][3];
 #pragma unroll
@@ -288,7 +289,10 @@ k_sketch_srht(const float4* __restrict__ pk, const uint32_t* __restrict__ tab, i
   for (int k = 0; k < TPO; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.f;
 
   for (int c = 0; c < A; ++c) {
-    // ---------------- phase A
+    float* W = Wbuf + (c & 1) * kSrhtSmemFloats;
+    float* wA = W + oA;
+    float* wB = W + oB;
+    // ---------------- phase A (writes the other buffer than chunk c-1's phase C reads: no barrier before it)
     {
       const float4* pc = pk + (int64_t)c * kSrhtB + cg;
       float v[2][16];
@@ -342,7 +346,6 @@ k_sketch_srht(const float4* __restrict__ pk, const uint32_t* __restrict__ tab, i
       acc[k][2] = fmaf(sg, w.z, acc[k][2]);
       acc[k][3] = fmaf(sg, w.w, acc[k][3]);
     }
-    __syncthreads();
   }
   // ---------------- epilogue: scale, nugget (by index, reading L9), store.
 #pragma unroll
@@ -368,8 +371,10 @@ template <int DIM, int KIND, int TPG>
 static ks_status launch_srht(const SketchLayout& L, const ks_sketch_desc& D, int64_t rb, int64_t re, float* Y,
                              char* ws, cudaStream_t st) {
   auto kern = k_sketch_srht<DIM, KIND, TPG>;
+  const int smem = 2 * kSrhtSmemFloats * (int)sizeof(float);
+  KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = (unsigned)((re - rb + kSrhtRows - 1) / kSrhtRows);
-  kern<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(ws + L.off_pk),
+  kern<<<grid, 256, smem, st>>>(reinterpret_cast<const float4*>(ws + L.off_pk),
                                 reinterpret_cast<const uint32_t*>(ws + L.off_tab), rb, re, L.A, D.d,
                                 (float)(1.0 / std::sqrt((double)L.N)), D.nugget, Y);
   KS_LAUNCH_CHECK();
