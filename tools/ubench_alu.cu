@@ -37,6 +37,22 @@ __global__ void kern(float* out, float s0, float s1, long long* clk) {
       }
       if (OP == 6) u[c] = (u[c] & 0xFFFFE000u) ^ (u[c] >> 3);          // LOP3 + SHF
       if (OP == 7) a[c] = a[c] - b[c] * b[c];                           // FFMA with shared operand
+      if (OP == 8 && (c & 1) == 0) {                                    // FADD2 (packed f32x2)
+        unsigned long long x, y;
+        asm volatile("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a[c]), "f"(a[c + 1]));
+        asm volatile("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b[c]), "f"(b[c + 1]));
+        asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
+        asm volatile("mov.b64 {%0, %1}, %2;" : "=f"(a[c]), "=f"(a[c + 1]) : "l"(x));
+      }
+      if (OP == 9 && (c & 1) == 0) {                                    // FFMA2 (packed f32x2)
+        unsigned long long x, y, z;
+        asm volatile("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a[c]), "f"(a[c + 1]));
+        asm volatile("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b[c]), "f"(b[c + 1]));
+        asm volatile("mov.b64 %0, {%1, %2};" : "=l"(z) : "f"(b[(c + 2) % kChains]), "f"(b[(c + 3) % kChains]));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x) : "l"(y), "l"(z));
+        asm volatile("mov.b64 {%0, %1}, %2;" : "=f"(a[c]), "=f"(a[c + 1]) : "l"(x));
+      }
+      if (OP == 10) a[c] = a[c] + b[(c + 1) % kChains] * 0.f + a[c] * 1e-7f; // mixed FFMA/FADD
     }
   }
   long long t1 = clock64();
@@ -85,5 +101,7 @@ int main() {
   run<5>("F2FP.PACK (+LOP)", 1);
   run<6>("LOP3+SHF (2 ops)", 2);
   run<7>("FFMA r,r,r (shared b)", 1);
+  run<8>("FADD2 f32x2 (2 flop-lanes)", 1);
+  run<9>("FFMA2 f32x2 (2 flop-lanes)", 1);
   return 0;
 }
