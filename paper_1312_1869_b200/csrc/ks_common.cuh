@@ -81,6 +81,43 @@ KS_DEVINL float cov_signed(const float (&xi)[3], const float4 p) {
   }
 }
 
+// ---------------------------------------------------------------- packed f32x2 (sm_100)
+// A pair of fp32 values in one 64-bit register pair; FADD2/FMUL2/FFMA2 process both halves with one
+// issue slot (round to nearest, like the scalar ops).  A scalar operand is broadcast with f2s(); ptxas
+// folds it into the instruction's .F32 operand modifier (no MOV).
+typedef unsigned long long f2_t;
+KS_DEVINL f2_t f2(float lo, float hi) { f2_t r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r; }
+KS_DEVINL f2_t f2s(float a) { return f2(a, a); }
+KS_DEVINL float f2lo(f2_t r) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); return a; }
+KS_DEVINL float f2hi(f2_t r) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); return b; }
+KS_DEVINL f2_t f2add(f2_t a, f2_t b) { f2_t r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+KS_DEVINL f2_t f2sub(f2_t a, f2_t b) { f2_t r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+KS_DEVINL f2_t f2mul(f2_t a, f2_t b) { f2_t r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+KS_DEVINL f2_t f2fma(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// K[i0,j] s_j and K[i1,j] s_j for a row pair (packed coordinates xi2[c] = (x_i0c, x_i1c)) and one
+// packed point p = (scaled coords, amplitude); same arithmetic as cov_signed, per half.
+template <int DIM, int KIND>
+KS_DEVINL f2_t cov_signed2(const f2_t (&xi2)[3], const float4 p) {
+  const f2_t dx = f2sub(xi2[0], f2s(p.x));
+  f2_t r2 = f2mul(dx, dx);
+  if (DIM > 1) { const f2_t dy = f2sub(xi2[1], f2s(p.y)); r2 = f2fma(dy, dy, r2); }
+  if (DIM > 2) { const f2_t dz = f2sub(xi2[2], f2s(p.z)); r2 = f2fma(dz, dz, r2); }
+  if (KIND == KS_KERNEL_SQEXP) {
+    const f2_t e = f2(ex2_approx(-f2lo(r2)), ex2_approx(-f2hi(r2)));
+    return f2mul(e, f2s(p.w));
+  } else {
+    const f2_t z = f2(sqrt_approx(f2lo(r2)), sqrt_approx(f2hi(r2)));
+    const f2_t tz = f2mul(z, f2s(-1.4426950408889634f));
+    const f2_t e = f2(ex2_approx(f2lo(tz)), ex2_approx(f2hi(tz)));
+    return f2mul(f2fma(z, f2s(p.w), f2s(p.w)), e);
+  }
+}
+
 }  // namespace ks
 
 // ----------------------------------------------------------------- host side

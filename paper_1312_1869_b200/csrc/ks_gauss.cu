@@ -29,7 +29,6 @@
 
 namespace ks {
 
-constexpr int kGStages = 3;
 constexpr int kGaussSegKb = 16;   // 1024 columns of K per TMEM accumulation segment
 constexpr int kGThreads = 512;
 constexpr int kATileBytes = kGaussBM * kGaussBK * 2;  // 16 KB per fp16 half
@@ -60,13 +59,6 @@ KS_DEVINL void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta
 KS_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 KS_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-KS_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B (SBO), LBO = 16 B (unused),
 // version 1 (sm_100), base offset 0 (tiles are 1024-aligned).
@@ -75,25 +67,6 @@ KS_DEVINL uint64_t umma_desc_sw128(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-KS_DEVINL void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
-}
-KS_DEVINL void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-KS_DEVINL void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
-}
 
 KS_DEVINL uint32_t pack_half2(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);
@@ -112,191 +85,50 @@ KS_DEVINL void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
 }
 
-// fp32 -> (hi, lo) fp16 pair with hi = x truncated to 10 fraction bits (exact in fp16 for the
-// normal range) and lo = fp16_RN(x - hi) (x - hi is exact in fp32): |x - hi - lo| <= 2^-21 |x|.
-KS_DEVINL void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const float ah = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-  const float bh = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
-  hi = pack_half2(ah, bh);
-  lo = pack_half2(a - ah, b - bh);
-}
 
-// ------------------------------------------------------------------ kernel
-// Warp roles (512 threads):
-//   warp 0      TMA producer of Omega^T tiles (one lane)
-//   warp 1      TMEM allocator + MMA issuer (one lane)
-//   warps 4-11  K-tile producers: 128 x 64 tile of S*K per stage, split hi/lo into SW128 smem
-//   warps 12-15 accumulator drainers (warp 12+q owns TMEM lanes 32q..32q+31 = rows of the tile)
-// The column loop is cut into segments of seg_kb stages.  Segment g accumulates
-//   acc[g & 1] = sum_{stages of g} (K_hi + K_lo) Omega        (both MMAs into ONE accumulator)
-// in TMEM (2 x DN columns, double buffered) and the drainers add it to Y in fp32 (round to nearest)
-// while the MMA runs the next segment: the tensor core's own fp32 accumulation only ever spans
-// 8*seg_kb MMAs, which bounds its (non round-to-nearest) accumulation error.
+
+// fp32 -> (hi, lo) fp16 pair: hi = x truncated to 10 fraction bits (exact in fp16 for the normal range),
+// lo = fp16_RN(x - hi) (x - hi is exact in fp32), so |x - hi - lo| <= 2^-21 |x|.
+// One producer thread's share of a stage: rows 4rq..4rq+3 (two packed row pairs) x columns j0..j0+7 of
+// S*K, split hi/lo and stored in the UMMA K-major SW128 layout.  The covariance and the lo = x - hi
+// subtraction run on packed f32x2 row pairs (one issue slot per two rows).
 template <int DIM, int KIND>
-__global__ void __launch_bounds__(kGThreads, 1)
-k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict__ pk, int64_t row_begin,
-               int64_t row_end, int nkb, int seg_kb, int DN, float nugget, float out_scale, float* __restrict__ Y) {
-  const int kBTileBytes = DN * kGaussBK * 2;
-  const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* a_hi = smem;
-  uint8_t* a_lo = smem + kGStages * kATileBytes;
-  uint8_t* b_t = a_lo + kGStages * kATileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b_t + kGStages * kBTileBytes);  // full[S], empty[S], accf[2], acce[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kGStages + 4);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row0 = row_begin + (int64_t)blockIdx.x * kGaussBM;
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kGStages);
-  const uint32_t accf0 = smem_u32(bars + 2 * kGStages), acce0 = smem_u32(bars + 2 * kGStages + 2);
-  const int nseg = (nkb + seg_kb - 1) / seg_kb;
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kGStages; ++s) {
-      mbar_init(full0 + 8 * s, 8 + 1);
-      mbar_init(empty0 + 8 * s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(accf0 + 8 * b, 1);
-      mbar_init(acce0 + 8 * b, 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer: Omega^T tiles (DN x 64)
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kGStages;
-        const uint32_t ph = (kb / kGStages) & 1;
-        mbar_wait(empty0 + 8 * s, ph ^ 1);
-        mbar_arrive_tx(full0 + 8 * s, kBTileBytes);
-        tma_load_2d(smem_u32(b_t + s * kBTileBytes), &tmB, kb * kGaussBK, 0, full0 + 8 * s);
+KS_DEVINL void produce_tile(const f2_t (&xi2)[2][3], const int64_t (&irow)[4], const float4 (&pts)[8], int64_t j0,
+                            bool diag, float nugget, uint8_t* a_hi, uint8_t* a_lo, int rq, int cq) {
+#pragma unroll
+  for (int pr = 0; pr < 2; ++pr) {
+    f2_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = cov_signed2<DIM, KIND>(xi2[pr], pts[q]);
+    if (diag) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float a = f2lo(v[q]), b = f2hi(v[q]);
+        if (j0 + q == irow[2 * pr]) a += nugget;       // nugget by index (reading L9)
+        if (j0 + q == irow[2 * pr + 1]) b += nugget;
+        v[q] = f2(a, b);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      // kind::f16 instruction descriptor: D=f32 (bit 4), A=B=f16, both K-major, N>>3 at 17, M>>4 at 24.
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(DN >> 3) << 17) | ((uint32_t)(kGaussBM >> 4) << 24);
-      for (int g = 0; g < nseg; ++g) {
-        const int buf = g & 1;
-        mbar_wait(acce0 + 8 * buf, ((g >> 1) & 1) ^ 1);  // drainers done with this buffer's previous use
-        tc_fence_after();
-        const uint32_t dtm = tmem + (uint32_t)(buf * DN);
-        const int kb1 = min(nkb, (g + 1) * seg_kb);
-        for (int kb = g * seg_kb; kb < kb1; ++kb) {
-          const int s = kb % kGStages;
-          const uint32_t ph = (kb / kGStages) & 1;
-          mbar_wait(full0 + 8 * s, ph);
-          tc_fence_after();
-          const uint64_t dh = umma_desc_sw128(smem_u32(a_hi + s * kATileBytes));
-          const uint64_t dl = umma_desc_sw128(smem_u32(a_lo + s * kATileBytes));
-          const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBTileBytes));
+    uint32_t hi[2][4], lo[2][4];
 #pragma unroll
-          for (int kk = 0; kk < kGaussBK / 16; ++kk) {
-            umma_f16(dtm, dh + 2 * kk, db + 2 * kk, idesc, (kb != g * seg_kb || kk != 0) ? 1u : 0u);
-            umma_f16(dtm, dl + 2 * kk, db + 2 * kk, idesc, 1u);   // +32 B per K=16 step
-          }
-          umma_commit(empty0 + 8 * s);
-        }
-        umma_commit(accf0 + 8 * buf);
-      }
+    for (int q = 0; q < 8; q += 2) {
+      const f2_t h0 = f2(__uint_as_float(__float_as_uint(f2lo(v[q])) & 0xFFFFE000u),
+                         __uint_as_float(__float_as_uint(f2hi(v[q])) & 0xFFFFE000u));
+      const f2_t h1 = f2(__uint_as_float(__float_as_uint(f2lo(v[q + 1])) & 0xFFFFE000u),
+                         __uint_as_float(__float_as_uint(f2hi(v[q + 1])) & 0xFFFFE000u));
+      const f2_t l0 = f2sub(v[q], h0), l1 = f2sub(v[q + 1], h1);   // exact in fp32
+      hi[0][q >> 1] = pack_half2(f2lo(h0), f2lo(h1));
+      hi[1][q >> 1] = pack_half2(f2hi(h0), f2hi(h1));
+      lo[0][q >> 1] = pack_half2(f2lo(l0), f2lo(l1));
+      lo[1][q >> 1] = pack_half2(f2hi(l0), f2hi(l1));
     }
-  } else if (warp >= 4 && warp < 12) {
-    // ---------------- K-tile producers: thread p -> rows 4rq..4rq+3, columns 8cq..8cq+7 of the tile
-    const int p = threadIdx.x - 128;
-    const int rq = p >> 3, cq = p & 7;
-    float xi[4][3];
-    int64_t irow[4];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      int64_t i = row0 + 4 * rq + rr;
-      irow[rr] = i;
-      if (i >= row_end) i = row_end - 1;
-      const float4 q = pk[i];
-      xi[rr][0] = q.x; xi[rr][1] = q.y; xi[rr][2] = q.z;
+    for (int h = 0; h < 2; ++h) {
+      const int r = 4 * rq + 2 * pr + h;
+      const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
+      *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(hi[h][0], hi[h][1], hi[h][2], hi[h][3]);
+      *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[h][0], lo[h][1], lo[h][2], lo[h][3]);
     }
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kGStages;
-      const uint32_t ph = (kb / kGStages) & 1;
-      const int64_t j0 = (int64_t)kb * kGaussBK + 8 * cq;
-      float4 pts[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) pts[q] = __ldg(pk + j0 + q);
-      mbar_wait(empty0 + 8 * s, ph ^ 1);
-      const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = cov_signed<DIM, KIND>(xi[rr], pts[q]);
-        if (diag) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (j0 + q == irow[rr]) v[q] += nugget;   // nugget by index (reading L9)
-        }
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) split2(v[2 * q], v[2 * q + 1], hi[q], lo[q]);
-        const int r = 4 * rq + rr;
-        const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(a_hi + s * kATileBytes + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(a_lo + s * kATileBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(full0 + 8 * s);
-    }
-  } else if (warp >= 12) {
-    // ---------------- drainers: Y[row, :] (+)= acc[g & 1][row, :] in fp32, scaled after the last segment
-    const int quarter = warp & 3;
-    const int row = 32 * quarter + lane;
-    const int64_t i = row0 + row;
-    const bool ok = i < row_end;
-    float* yr = Y + (i - row_begin) * (int64_t)DN;
-    const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
-    for (int g = 0; g < nseg; ++g) {
-      const int buf = g & 1;
-      mbar_wait(accf0 + 8 * buf, (g >> 1) & 1);
-      tc_fence_after();
-      const bool first = g == 0, last = g == nseg - 1;
-      for (int c0 = 0; c0 < DN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tl + (uint32_t)(buf * DN + c0), v);
-        if (ok) {
-          float4* dst = reinterpret_cast<float4*>(yr + c0);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float4 a = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            if (!first) {
-              const float4 o = dst[q];
-              a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
-            }
-            if (last) { a.x *= out_scale; a.y *= out_scale; a.z *= out_scale; a.w *= out_scale; }
-            dst[q] = a;
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acce0 + 8 * buf);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -309,6 +141,8 @@ k_sketch_gauss(const __grid_constant__ CUtensorMap tmB, const float4* __restrict
 // complete_tx on it) and acce[b] (drainers of both CTAs arrive); its commits multicast to both CTAs'
 // empty[s] / accf[b].
 constexpr int kG2Stages = 4;
+constexpr int kPtsStages = 8;                       // ring of the stages' packed points (1 KB each)
+constexpr int kPtsBytes = kGaussBK * 16;
 
 KS_DEVINL uint32_t cluster_rank() {
   uint32_t r;
@@ -323,20 +157,17 @@ KS_DEVINL uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
 KS_DEVINL void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-KS_DEVINL void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  }
-}
+// Remote arrive on the leader's barrier.  Default (.release.cta) semantics, as CUTLASS's ClusterBarrier: the
+// .release.cluster form costs a MEMBAR.ALL.GPU per arrive, and the producers' smem writes reach the
+// leader's MMA through fence.proxy.async + the barrier (waited on by the MMA thread), not through L1.
 KS_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 1-D bulk copy global -> own shared memory, completing on an mbarrier of this CTA.
+KS_DEVINL void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
 }
 KS_DEVINL void tma_load_2d_2cta(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar_cluster) {
   asm volatile(
@@ -370,14 +201,17 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
   uint8_t* a_hi = smem;
   uint8_t* a_lo = smem + kG2Stages * kATileBytes;
   uint8_t* b_t = a_lo + kG2Stages * kATileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b_t + kG2Stages * kBHalfBytes);  // full[S], empty[S], accf[2], acce[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kG2Stages + 4);
+  float4* pring = reinterpret_cast<float4*>(b_t + kG2Stages * kBHalfBytes);     // [kPtsStages][64] points
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pring + kPtsStages * kGaussBK);
+  // full[S], empty[S], accf[2], acce[2], pfull[PS], pempty[PS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kG2Stages + 4 + 2 * kPtsStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int64_t row0 = row_begin + (int64_t)(blockIdx.x >> 1) * 256 + 128 * (int64_t)rank;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kG2Stages);
   const uint32_t accf0 = smem_u32(bars + 2 * kG2Stages), acce0 = smem_u32(bars + 2 * kG2Stages + 2);
+  const uint32_t pfull0 = smem_u32(bars + 2 * kG2Stages + 4), pempty0 = pfull0 + 8 * kPtsStages;
   const uint32_t full0_L = mapa_u32(full0, 0), acce0_L = mapa_u32(acce0, 0);   // the leader's barriers
   const int nseg = (nkb + seg_kb - 1) / seg_kb;
 
@@ -389,6 +223,10 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
     for (int b = 0; b < 2; ++b) {
       mbar_init(accf0 + 8 * b, 1);
       mbar_init(acce0 + 8 * b, 8);         // 4 drain warps x 2 CTAs
+    }
+    for (int s = 0; s < kPtsStages; ++s) {
+      mbar_init(pfull0 + 8 * s, 1);
+      mbar_init(pempty0 + 8 * s, 8);       // the 8 producer warps of this CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -408,9 +246,19 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % kG2Stages;
         const uint32_t ph = (kb / kG2Stages) & 1;
-        mbar_wait_cluster(empty0 + 8 * s, ph ^ 1);
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
         if (rank == 0) mbar_arrive_tx(full0 + 8 * s, 2 * kBHalfBytes);
         tma_load_2d_2cta(smem_u32(b_t + s * kBHalfBytes), &tmB, kb * kGaussBK, (int)rank * (DN / 2), full0_L + 8 * s);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {  // ---------------- points loader: the stage's 64 packed points, kPtsStages ahead
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kPtsStages;
+        const uint32_t ph = (kb / kPtsStages) & 1;
+        mbar_wait(pempty0 + 8 * s, ph ^ 1);
+        mbar_arrive_tx(pfull0 + 8 * s, kPtsBytes);
+        bulk_load(smem_u32(pring + s * kGaussBK), pk + (int64_t)kb * kGaussBK, kPtsBytes, pfull0 + 8 * s);
       }
     }
   } else if (warp == 1) {
@@ -418,14 +266,14 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
       const uint32_t idesc = (1u << 4) | ((uint32_t)(DN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
       for (int g = 0; g < nseg; ++g) {
         const int buf = g & 1;
-        mbar_wait_cluster(acce0 + 8 * buf, ((g >> 1) & 1) ^ 1);
+        mbar_wait(acce0 + 8 * buf, ((g >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dtm = tmem + (uint32_t)(buf * DN);
         const int kb1 = min(nkb, (g + 1) * seg_kb);
         for (int kb = g * seg_kb; kb < kb1; ++kb) {
           const int s = kb % kG2Stages;
           const uint32_t ph = (kb / kG2Stages) & 1;
-          mbar_wait_cluster(full0 + 8 * s, ph);
+          mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
           const uint64_t dh = umma_desc_sw128(smem_u32(a_hi + s * kATileBytes));
           const uint64_t dl = umma_desc_sw128(smem_u32(a_lo + s * kATileBytes));
@@ -444,43 +292,34 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
     // ---------------- K-tile producers: thread p -> rows 4rq..4rq+3, columns 8cq..8cq+7 of the tile
     const int p = threadIdx.x - 128;
     const int rq = p >> 3, cq = p & 7;
-    float xi[4][3];
+    f2_t xi2[2][3];
     int64_t irow[4];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      int64_t i = row0 + 4 * rq + rr;
-      irow[rr] = i;
-      if (i >= row_end) i = row_end - 1;
-      const float4 q = pk[i];
-      xi[rr][0] = q.x; xi[rr][1] = q.y; xi[rr][2] = q.z;
+    for (int pr = 0; pr < 2; ++pr) {
+      float4 q[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int64_t i = row0 + 4 * rq + 2 * pr + h;
+        irow[2 * pr + h] = i;
+        if (i >= row_end) i = row_end - 1;
+        q[h] = pk[i];
+      }
+      xi2[pr][0] = f2(q[0].x, q[1].x); xi2[pr][1] = f2(q[0].y, q[1].y); xi2[pr][2] = f2(q[0].z, q[1].z);
     }
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kG2Stages;
       const uint32_t ph = (kb / kG2Stages) & 1;
       const int64_t j0 = (int64_t)kb * kGaussBK + 8 * cq;
+      const int ps = kb % kPtsStages;
+      mbar_wait(pfull0 + 8 * ps, (kb / kPtsStages) & 1);
       float4 pts[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) pts[q] = __ldg(pk + j0 + q);
-      mbar_wait_cluster(empty0 + 8 * s, ph ^ 1);
+      for (int q = 0; q < 8; ++q) pts[q] = pring[ps * kGaussBK + 8 * cq + q];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pempty0 + 8 * ps);   // release: this warp's reads of the slot are done
+      mbar_wait(empty0 + 8 * s, ph ^ 1);
       const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = cov_signed<DIM, KIND>(xi[rr], pts[q]);
-        if (diag) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (j0 + q == irow[rr]) v[q] += nugget;   // nugget by index (reading L9)
-        }
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) split2(v[2 * q], v[2 * q + 1], hi[q], lo[q]);
-        const int r = 4 * rq + rr;
-        const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(a_hi + s * kATileBytes + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(a_lo + s * kATileBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
+      produce_tile<DIM, KIND>(xi2, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(full0_L + 8 * s);
@@ -495,7 +334,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
     const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
     for (int g = 0; g < nseg; ++g) {
       const int buf = g & 1;
-      mbar_wait_cluster(accf0 + 8 * buf, (g >> 1) & 1);
+      mbar_wait(accf0 + 8 * buf, (g >> 1) & 1);
       tc_fence_after();
       const bool first = g == 0, last = g == nseg - 1;
       for (int c0 = 0; c0 < DN; c0 += 64) {   // 64 columns per batch: all of Y's loads in flight together
@@ -571,18 +410,12 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   auto encode = get_encode();
   if (!encode) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int DN = D.d;
-  CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)L.ncols_pad, (cuuint64_t)DN};
   cuuint64_t strides[1] = {(cuuint64_t)L.ncols_pad * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kGaussBK, (cuuint32_t)DN};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ws + L.off_gauss, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   CUtensorMap tm2;   // half-width boxes (DN/2 rows of Omega^T) for the CTA pair
   cuuint32_t box2[2] = {(cuuint32_t)kGaussBK, (cuuint32_t)(DN / 2)};
-  r = encode(&tm2, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ws + L.off_gauss, dims, strides, box2, estr,
+  CUresult r = encode(&tm2, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ws + L.off_gauss, dims, strides, box2, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -590,20 +423,11 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   const double S = gauss_scale(D);
   const float nug = (float)(S * D.nugget), osc = (float)(1.0 / (S * std::sqrt((double)D.d)));
   const float4* pk = reinterpret_cast<const float4*>(ws + L.off_pk);
-  static const bool one_cta = [] { const char* e = getenv("KS_GAUSS_1CTA"); return e && atoi(e) > 0; }();
-  if (one_cta) {
-    const int smem = 1024 + kGStages * (2 * kATileBytes + DN * kGaussBK * 2) + 256;
-    auto kern = k_sketch_gauss<DIM, KIND>;
-    KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const unsigned grid = (unsigned)((re - rb + kGaussBM - 1) / kGaussBM);
-    kern<<<grid, kGThreads, smem, st>>>(tm, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
-  } else {
-    const int smem = 1024 + kG2Stages * (2 * kATileBytes + (DN / 2) * kGaussBK * 2) + 256;
-    auto kern = k_sketch_gauss2<DIM, KIND>;
-    KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const unsigned grid = 2u * (unsigned)((re - rb + 255) / 256);
-    kern<<<grid, kGThreads, smem, st>>>(tm2, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
-  }
+  const int smem = 1024 + kG2Stages * (2 * kATileBytes + (DN / 2) * kGaussBK * 2) + kPtsStages * kPtsBytes + 512;
+  auto kern = k_sketch_gauss2<DIM, KIND>;
+  KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const unsigned grid = 2u * (unsigned)((re - rb + 255) / 256);
+  kern<<<grid, kGThreads, smem, st>>>(tm2, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }

@@ -37,17 +37,17 @@ void count_launch();
 
 // ---------------------------------------------------------------- sketch side
 constexpr int kSrhtB = 512;         // SRHT chunk length (columns of K per transform block)
-constexpr int kSrhtRows = 16;       // rows of Y per CTA
+constexpr int kSrhtRows = 8;        // rows of Y per sketch CTA (128 threads, 4 CTAs per SM)
 constexpr int kGaussBM = 128;       // rows per tcgen05 tile
 constexpr int kGaussBK = 64;        // reduction (j) block per pipeline stage
 
 struct SketchLayout {
   int64_t N;          // 2^ceil(log2 n)
   int64_t ncols_pad;  // packed-point count (multiple of the chunk length)
-  int A;              // number of SRHT chunks covering [0, n)
-  int d_pad;          // SRHT: outputs padded to 32 * TPG
-  int tpg;            // SRHT outputs per thread group
-  size_t off_pk, off_tab, off_sel, off_bucket_ofs, off_bucket_idx, off_bitmap, off_gauss, bytes;
+  int A;              // number of kSrhtB-chunks covering [0, n) (Omega-apply)
+  int tpo;            // SRHT sketch: outputs per thread in the gather phase
+  int d_pad;          // SRHT sketch: output slots, 64 * tpo (slot -> output by the perm table)
+  size_t off_pk, off_tab, off_sel, off_bucket_ofs, off_bucket_idx, off_bitmap, off_gauss, off_perm, off_sgn, bytes;
 };
 
 ks_status sketch_validate(const ks_sketch_desc* desc);

@@ -9,10 +9,13 @@
 //   j = c*B + l,  S_t = a_t*B + m_t:
 //   Y[i, t] = (1/sqrt N) sum_c (-1)^popc(c & a_t) * FWHT_B(s o K[i, cB : cB+B])[m_t]
 //
-// i.e. every chunk of B columns is transformed completely (log2 B butterfly
-// levels, 4 in registers + 5 after one shared-memory transpose) and the d
-// selected outputs are gathered with the chunk's sign -- N (log2 B + d/B)
-// adds per row, the "n log d" of PAPER.md:19, instead of N log2 N.
+// i.e. every chunk of B columns is transformed (log2 B butterfly levels: 4 in
+// registers, 5 after one shared-memory exchange) and the d selected outputs are
+// gathered with the chunk's sign --
+// N (log2 B + d/B) adds per row, the "n log d" of PAPER.md:19, instead of N log2 N.
+// All arithmetic on row PAIRS uses Blackwell's packed f32x2 instructions
+// (FADD2/FMUL2/FFMA2): the FP32 pipe does the same lane-ops, but each instruction
+// issues once for two rows, so the kernel is bound by the FP32 pipe, not by issue.
 #include "ks_common.cuh"
 #include "ks_internal.h"
 
@@ -28,15 +31,15 @@ SketchLayout sketch_layout(const ks_sketch_desc& desc) {
   if (desc.omega == KS_OMEGA_SRHT) {
     L.A = (int)((desc.n + kSrhtB - 1) / kSrhtB);
     L.ncols_pad = (int64_t)L.A * kSrhtB;
-    int tpg = 2;
-    while (32 * tpg < desc.d) tpg *= 2;
-    L.tpg = tpg;
-    L.d_pad = 32 * tpg;
+    int tpo = 1;
+    while (64 * tpo < desc.d) tpo *= 2;   // 64 output groups in the gather phase
+    L.tpo = tpo;
+    L.d_pad = 64 * tpo;
   } else {
     L.A = 0;
     L.ncols_pad = (desc.n + kGaussBK - 1) / kGaussBK * kGaussBK;
     if (L.ncols_pad < kGaussBM) L.ncols_pad = kGaussBM;
-    L.tpg = 0;
+    L.tpo = 0;
     L.d_pad = desc.d;
   }
   // Row points are read from the same packed array; rows beyond n never occur.
@@ -49,6 +52,8 @@ SketchLayout sketch_layout(const ks_sketch_desc& desc) {
   L.off_bucket_idx = take(sizeof(int32_t) * 512);
   L.off_bitmap = take(sizeof(uint32_t) * (size_t)((L.N + 31) / 32));
   L.off_gauss = take(desc.omega == KS_OMEGA_GAUSS ? sizeof(__half) * (size_t)desc.d * (size_t)L.ncols_pad : 0);
+  L.off_perm = take(desc.omega == KS_OMEGA_SRHT ? sizeof(int32_t) * (size_t)L.d_pad : 0);
+  L.off_sgn = take(desc.omega == KS_OMEGA_SRHT ? sizeof(float) * (size_t)L.A * (size_t)L.d_pad : 0);
   L.bytes = off;
   return L;
 }
@@ -97,98 +102,170 @@ __global__ void k_pack_points(const float* __restrict__ pts, int64_t n, int dim,
   pk[j] = p;
 }
 
-// Selection S: the first d distinct values of (philox(seed, 2, t).x & (N-1)), t = 0, 1, ...
-// (uniform without replacement, reading L4), sorted ascending.  One CTA of 1024 threads;
-// also writes the SRHT gather table and the (m_t)-bucket CSR used by the Omega-apply.
-__global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, int d, int d_pad,
-                                                    uint32_t* __restrict__ bitmap, int32_t* __restrict__ sel,
+// Exclusive block scan of a 0/1 flag over 1024 threads: returns the rank, *total = number of flags.
+KS_DEVINL int block_rank(bool flag, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(0xffffffffu, flag);
+  __syncthreads();   // wsum reuse
+  if (lane == 0) wsum[wid] = __popc(b);
+  __syncthreads();
+  if (wid == 0) {
+    int v = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int u = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v += u; }
+    wsum[lane] = v;   // inclusive
+  }
+  __syncthreads();
+  *total = wsum[31];
+  return (wid ? wsum[wid - 1] : 0) + __popc(b & ((1u << lane) - 1u));
+}
+
+// Selection S (reading L4): the first d distinct values of (philox(seed, 2, t).x & (N-1)), t = 0, 1, ...,
+// sorted ascending.  Warp 0 scans the stream 32 draws at a time (__match_any_sync finds duplicates inside
+// the round, a bitmap of N bits -- in shared memory when N <= 2^20 -- the earlier ones), then all 1024
+// threads enumerate the bitmap in order.  Also builds, for the sketch and the Omega-apply:
+//   tab[t]  = m_t | a_t << 16 (kSrhtB-chunks),
+//   bofs/bidx = CSR of t by bucket m_t, ascending t inside a bucket,
+//   perm[s] = the gather slot permutation of the sketch: slot s = og*tpo + k prefers outputs whose F row
+//             sits in the 8-bank group cls(m) = (m + (m >> 5)) & 3 equal to og & 3, so the four groups of a
+//             quarter-warp read distinct banks; outputs left over fill the remaining slots in order.
+constexpr int64_t kSelSmemBits = int64_t(1) << 20;
+__global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, int d, int d_pad, int tpo,
+                                                    uint32_t* __restrict__ gbitmap, int32_t* __restrict__ sel,
                                                     uint32_t* __restrict__ tab, int32_t* __restrict__ bofs,
-                                                    int32_t* __restrict__ bidx) {
-  __shared__ uint32_t cand[1024];
-  __shared__ int warp_sums[32];
-  __shared__ int s_count;
+                                                    int32_t* __restrict__ bidx, int32_t* __restrict__ perm) {
+  extern __shared__ uint32_t sbits[];   // N/32 words when N <= 2^20
+  __shared__ int s_sel[512];
+  __shared__ int s_lst[4][512];         // outputs of each class, ascending t
+  __shared__ int s_left[512];
+  __shared__ int s_hist[kSrhtB + 1];
+  __shared__ int s_fill[kSrhtB];
+  __shared__ int wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool in_smem = N <= kSelSmemBits;
+  uint32_t* bitmap = in_smem ? sbits : gbitmap;
   const int64_t nwords = (N + 31) / 32;
   for (int64_t w = tid; w < nwords; w += 1024) bitmap[w] = 0u;
-  if (tid == 0) s_count = 0;
   __syncthreads();
-  for (uint64_t base = 0; s_count < d; base += 1024) {
-    const uint32_t c = philox(seed, kStreamSelect, base + (uint64_t)tid).x & (uint32_t)(N - 1);
-    cand[tid] = c;
-    __syncthreads();
-    bool isnew = !((bitmap[c >> 5] >> (c & 31)) & 1u);
-    for (int q = 0; q < tid && isnew; ++q) isnew = cand[q] != c;
-    // block exclusive scan of isnew
-    const unsigned ball = __ballot_sync(0xffffffffu, isnew);
-    const int in_warp = __popc(ball & ((1u << lane) - 1u));
-    if (lane == 0) warp_sums[wid] = __popc(ball);
-    __syncthreads();
-    if (wid == 0) {
-      int v = warp_sums[lane];
-      for (int o = 1; o < 32; o <<= 1) { int u = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v += u; }
-      warp_sums[lane] = v;  // inclusive
+  if (wid == 0) {
+    int count = 0;
+    for (uint64_t base = 0; count < d; base += 32) {
+      const uint32_t c = philox(seed, kStreamSelect, base + (uint64_t)lane).x & (uint32_t)(N - 1);
+      const unsigned same = __match_any_sync(0xffffffffu, c);
+      const uint32_t word = in_smem ? bitmap[c >> 5] : __ldcg(bitmap + (c >> 5));
+      const bool keep = (__ffs(same) - 1) == lane && !((word >> (c & 31)) & 1u);
+      const unsigned ball = __ballot_sync(0xffffffffu, keep);
+      const int pos = count + __popc(ball & ((1u << lane) - 1u));
+      if (keep && pos < d) atomicOr(bitmap + (c >> 5), 1u << (c & 31));
+      count = min(d, count + __popc(ball));
+      __syncwarp();
     }
-    __syncthreads();
-    const int excl = (wid ? warp_sums[wid - 1] : 0) + in_warp;
-    const int total = warp_sums[31];
-    const int remaining = d - s_count;
-    if (isnew && excl < remaining) atomicOr(&bitmap[c >> 5], 1u << (c & 31));
-    __syncthreads();
-    if (tid == 0) s_count += total < remaining ? total : remaining;
-    __syncthreads();
   }
-  // Sorted enumeration of the bitmap: contiguous word ranges per thread, block scan of counts.
+  __syncthreads();
+  // sorted enumeration: contiguous word ranges per thread, block scan of the counts
   const int64_t per = (nwords + 1023) / 1024;
   const int64_t w0 = (int64_t)tid * per, w1 = (w0 + per < nwords) ? w0 + per : nwords;
   int cnt = 0;
-  for (int64_t w = w0; w < w1; ++w) cnt += __popc(bitmap[w]);
+  for (int64_t w = w0; w < w1; ++w) cnt += __popc(in_smem ? bitmap[w] : __ldcg(bitmap + w));
   int v = cnt;
-  for (int o = 1; o < 32; o <<= 1) { int u = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v += u; }
-  if (lane == 31) warp_sums[wid] = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) { const int u = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v += u; }
+  if (lane == 31) wsum[wid] = v;
   __syncthreads();
   if (wid == 0) {
-    int x = warp_sums[lane];
-    for (int o = 1; o < 32; o <<= 1) { int u = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += u; }
-    warp_sums[lane] = x;
+    int x = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int u = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += u; }
+    wsum[lane] = x;
   }
   __syncthreads();
-  int pos = (wid ? warp_sums[wid - 1] : 0) + v - cnt;
+  int pos = (wid ? wsum[wid - 1] : 0) + v - cnt;
   for (int64_t w = w0; w < w1; ++w) {
-    uint32_t bits = bitmap[w];
+    uint32_t bits = in_smem ? bitmap[w] : __ldcg(bitmap + w);
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
-      sel[pos++] = (int32_t)(w * 32 + b);
+      s_sel[pos] = (int32_t)(w * 32 + b);
+      sel[pos] = (int32_t)(w * 32 + b);
+      ++pos;
+    }
+  }
+  for (int b = tid; b <= kSrhtB; b += 1024) s_hist[b] = 0;
+  if (tid < kSrhtB) s_fill[tid] = 0;
+  __syncthreads();
+  // ---- tab and the bucket CSR (counting sort by m_t, then each bucket sorted by t)
+  const bool act = tid < d;
+  const int st = act ? s_sel[tid] : 0;
+  const int m = st & (kSrhtB - 1);
+  if (act) {
+    tab[tid] = (uint32_t)m | ((uint32_t)(st / kSrhtB) << 16);
+    atomicAdd(&s_hist[m + 1], 1);
+  }
+  __syncthreads();
+  if (wid == 0) {   // exclusive offsets: s_hist[b] = first slot of bucket b (16 buckets per lane)
+    int loc[16], acc = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) { acc += s_hist[16 * lane + q + 1]; loc[q] = acc; }
+    int x = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int u = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += u; }
+    const int base = x - acc;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s_hist[16 * lane + q + 1] = base + loc[q];
+  }
+  __syncthreads();
+  for (int b = tid; b <= kSrhtB; b += 1024) bofs[b] = s_hist[b];
+  if (act) s_left[s_hist[m] + atomicAdd(&s_fill[m], 1)] = tid;
+  __syncthreads();
+  if (tid < kSrhtB) {   // insertion sort of each (tiny) bucket by t
+    const int b0 = s_hist[tid], b1 = s_hist[tid + 1];
+    for (int i = b0 + 1; i < b1; ++i) {
+      const int x = s_left[i];
+      int j = i - 1;
+      while (j >= b0 && s_left[j] > x) { s_left[j + 1] = s_left[j]; --j; }
+      s_left[j + 1] = x;
     }
   }
   __syncthreads();
-  // SRHT gather table: (m_t | a_t << 16), padded entries inert.
-  for (int t = tid; t < d_pad; t += 1024) {
-    uint32_t e = 0u;
-    if (t < d) {
-      const uint32_t s = (uint32_t)sel[t];
-      e = (s & (kSrhtB - 1)) | ((s / kSrhtB) << 16);
-    }
-    tab[t] = e;
-  }
-  // CSR of t by m_t (deterministic, ascending t within a bucket) for the Omega-apply.
-  if (tid == 0) {
-    for (int b = 0; b <= kSrhtB; ++b) bofs[b] = 0;
-    for (int t = 0; t < d; ++t) bofs[(sel[t] & (kSrhtB - 1)) + 1]++;
-    for (int b = 0; b < kSrhtB; ++b) bofs[b + 1] += bofs[b];
-    for (int t = 0; t < d; ++t) {
-      const int b = sel[t] & (kSrhtB - 1);
-      int p = bofs[b];
-      while (bidx[p] != -1 && p < bofs[b + 1]) ++p;  // first free slot (slots pre-marked -1 below)
-      bidx[p] = t;
-    }
-  }
+  if (act) bidx[tid] = s_left[tid];
+  // ---- perm
+  const int h = (m + (m >> 5)) & 3;
+  int rank[4], ncls[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) rank[c] = block_rank(act && h == c, wsum, &ncls[c]);
+  int myrank = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) myrank = (c == h) ? rank[c] : myrank;
+  if (act) s_lst[h][myrank] = tid;
+  const int per_cls = d_pad / 4;   // slots of each class
+  int nleft = 0;
+  const int lrank = block_rank(act && myrank >= per_cls, wsum, &nleft);   // (its barriers publish s_lst)
+  if (act && myrank >= per_cls) s_left[lrank] = tid;
+  // slot s: class og & 3, index inside its class (og >> 2) * tpo + k
+  const bool sact = tid < d_pad;
+  const int og = tid / tpo, kk = tid - og * tpo, want = og & 3, mi = (og >> 2) * tpo + kk;
+  int want_n = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) want_n = (c == want) ? ncls[c] : want_n;
+  const bool over = sact && mi >= want_n;
+  int nover = 0;
+  const int orank = block_rank(over, wsum, &nover);   // (its barriers publish s_left)
+  if (sact) perm[tid] = !over ? s_lst[want][mi] : (orank < nleft ? s_left[orank] : -1);
 }
 
-__global__ void k_fill_i32(int32_t* p, int n, int32_t v) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
+// Chunk signs of the sketch's gather: sgn[c][s] = (-1)^popc(c & a_t), t = perm[s], a_t = S_t / B; 0 for empty slots.
+__global__ void k_srht_signs(const int32_t* __restrict__ sel, const int32_t* __restrict__ perm, int d_pad, int A,
+                             float* __restrict__ sgn) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)A * d_pad) return;
+  const int c = (int)(p / d_pad), sl = (int)(p - (int64_t)c * d_pad);
+  const int t = perm[sl];
+  float v = 0.f;
+  if (t >= 0) v = (__popc((uint32_t)c & ((uint32_t)sel[t] / (uint32_t)kSrhtB)) & 1) ? -1.f : 1.f;
+  sgn[p] = v;
 }
+
 
 // Gaussian Omega^T (d x ncols_pad, fp16): Omega_jt = fp16_RN(z), z = Box-Muller(philox(seed, 3, j*d + t))
 // (reading L6); the 1/sqrt(d) is applied in the sketch epilogue.  Columns j >= n are zero.
@@ -224,13 +301,24 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
     KS_LAUNCH_CHECK();
   }
   if (srht) {
-    k_fill_i32<<<2, 256, 0, st>>>(reinterpret_cast<int32_t*>(ws + L.off_bucket_idx), 512, -1);
+    static bool attr = false;
+    if (!attr) {
+      KS_CUDA_TRY(cudaFuncSetAttribute(k_selection, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelSmemBits / 8)));
+      attr = true;
+    }
+    const int sel_smem = L.N <= kSelSmemBits ? (int)((L.N + 31) / 32 * 4) : 0;
+    k_selection<<<1, 1024, sel_smem, st>>>(D.seed, L.N, D.d, L.d_pad, L.tpo,
+                                           reinterpret_cast<uint32_t*>(ws + L.off_bitmap),
+                                           reinterpret_cast<int32_t*>(ws + L.off_sel),
+                                           reinterpret_cast<uint32_t*>(ws + L.off_tab),
+                                           reinterpret_cast<int32_t*>(ws + L.off_bucket_ofs),
+                                           reinterpret_cast<int32_t*>(ws + L.off_bucket_idx),
+                                           reinterpret_cast<int32_t*>(ws + L.off_perm));
     KS_LAUNCH_CHECK();
-    k_selection<<<1, 1024, 0, st>>>(D.seed, L.N, D.d, L.d_pad, reinterpret_cast<uint32_t*>(ws + L.off_bitmap),
-                                    reinterpret_cast<int32_t*>(ws + L.off_sel),
-                                    reinterpret_cast<uint32_t*>(ws + L.off_tab),
-                                    reinterpret_cast<int32_t*>(ws + L.off_bucket_ofs),
-                                    reinterpret_cast<int32_t*>(ws + L.off_bucket_idx));
+    const int64_t ns = (int64_t)L.A * L.d_pad;
+    k_srht_signs<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(reinterpret_cast<const int32_t*>(ws + L.off_sel),
+                                                               reinterpret_cast<const int32_t*>(ws + L.off_perm),
+                                                               L.d_pad, L.A, reinterpret_cast<float*>(ws + L.off_sgn));
     KS_LAUNCH_CHECK();
   } else {
     dim3 grid((unsigned)((L.ncols_pad + 255) / 256), (unsigned)D.d);
@@ -241,154 +329,176 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
 }
 
 // ============================================================ fused SRHT kernel
-// One CTA = 16 rows of Y (256 threads, 2-3 CTAs per SM); loops over the column chunks c of K.
-// The tile W is double buffered, so a chunk needs 2 barriers (after phase A, after phase B).
-// Shared tile W: column l (0..511) of the chunk holds its 16 row values at
-// A(l, r) = l*16 + (l >> 5)*16 + r (the (l >> 5) pad makes phase B conflict-free).
-//   phase A : thread (rg = t&7, cg = t>>3) evaluates K*s for rows 2rg, 2rg+1 and columns
-//             l = cg + 32q, q < 16, butterflies over l bits 5-8 in registers, stores W.
-//   phase B : thread (rp = t&15, g = t>>4) loads row rp at l = 32g + b, b < 32, butterflies
-//             over l bits 0-4, stores back.  W now holds FWHT_B of the chunk (natural order).
-//   phase C : thread (rq = t&3, og = t>>2) accumulates its TPO = TPG/2 outputs for rows
-//             4rq..4rq+3: acc[k] += (-1)^popc(c & a_t) * W[m_t][4rq .. 4rq+3].
-KS_DEVINL int srht_w(int l, int r) { return l * 16 + (l >> 5) * 16 + r; }
-constexpr int kSrhtSmemFloats = kSrhtB * 16 + (kSrhtB / 32) * 16;   // 33 KB per buffer
+// One CTA = 8 rows of Y (128 threads, 4 CTAs per SM, whose phases interleave); loops over the column
+// chunks c of K.  The tile W is double buffered, so a chunk needs 2 barriers (after phase A, after B).
+// Shared tile W: column l (0..511) of the chunk holds its 8 row values at
+// A(l, r) = l*8 + (l >> 5)*8 + r (the (l >> 5) pad makes phase B conflict-free).
+//   phase A : thread (rg = t&3, cg = t>>2) evaluates K*s for the row pair 2rg, 2rg+1 (packed f32x2)
+//             at columns l = cg + 32q, q < 16, butterflies over l bits 5-8 in registers, stores W.
+//   phase B : thread (rp = t&7, g = t>>3) loads row rp at l = 32g + b, b < 32, into register pairs
+//             (b, b+16), butterflies over l bits 0-3 (packed) and bit 4, stores back.  W now holds
+//             FWHT_B of the chunk (natural order).
+//   phase C : thread (rq = t&1, og = t>>1) accumulates its TPO gather slots s = og*TPO + k (output
+//             t = perm[s]) for rows 4rq..4rq+3: acc += sgn[c][s] * W[m_t][4rq .. 4rq+3] (packed).
+// Packed f32x2 arithmetic issues once per row pair: the FP32 pipe does the same lane-ops, but the
+// kernel is no longer bound by issue slots.  The chunk's packed points are staged in shared memory
+// by cp.async one chunk ahead.
+constexpr int kSrhtThreads = 128;
+KS_DEVINL int srht_w(int l, int r) { return l * 8 + (l >> 5) * 8 + r; }
+constexpr int kSrhtSmemFloats = kSrhtB * 8 + (kSrhtB / 32) * 8;   // 16.5 KB per buffer
+constexpr int kSrhtSmemBytes = 2 * kSrhtSmemFloats * 4 + 2 * kSrhtB * 16;   // + 2 x 8 KB point tiles
 
-template <int DIM, int KIND, int TPG>
-__global__ void __launch_bounds__(256, TPG <= 8 ? 3 : 2)
-k_sketch_srht(const float4* __restrict__ pk, const uint32_t* __restrict__ tab, int64_t row_begin, int64_t row_end,
-              int A, int d, float out_scale, float nugget, float* __restrict__ Y) {
-  constexpr int TPO = TPG / 2;
-  extern __shared__ __align__(16) float Wbuf[];   // [2][kSrhtSmemFloats], double buffered: chunk c uses half c & 1
+KS_DEVINL void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+KS_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+KS_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int DIM, int KIND, int TPO>
+__global__ void __launch_bounds__(kSrhtThreads, 4)
+k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, const int32_t* __restrict__ perm,
+              const float* __restrict__ sgn, int64_t row_begin, int64_t row_end, int A, int d, int d_pad,
+              float out_scale, float nugget, float* __restrict__ Y) {
+  extern __shared__ __align__(16) float Wbuf[];   // [2][kSrhtSmemFloats], chunk c uses half c & 1
+  float4* Pbuf = reinterpret_cast<float4*>(Wbuf + 2 * kSrhtSmemFloats);   // [2][kSrhtB] packed points
   const int t = threadIdx.x;
-  const int rg = t & 7, cg = t >> 3;
-  const int rp = t & 15, g = t >> 4;
-  const int rq = t & 3, og = t >> 2;
+  const int rg = t & 3, cg = t >> 2;
+  const int rp = t & 7, g = t >> 3;
+  const int rq = t & 1, og = t >> 1;
   const int64_t row0 = row_begin + (int64_t)blockIdx.x * kSrhtRows;
-  const int oA = cg * 16 + 2 * rg;         // + 528 q           (= srht_w(cg + 32 q, 2 rg))
-  const int oB = 528 * g + rp;             // + 16 b            (= srht_w(32 g + b, rp))
+  const int oA = srht_w(cg, 2 * rg);       // + 264 q   (= srht_w(cg + 32 q, 2 rg))
+  const int oB = 264 * g + rp;             // + 8 b     (= srht_w(32 g + b, rp))
 
-  float xi[2][3];
-#pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    int64_t i = row0 + 2 * rg + rr;
-    if (i >= row_end) i = row_end - 1;
-    const float4 p = pk[i];
-    xi[rr][0] = p.x; xi[rr][1] = p.y; xi[rr][2] = p.z;
+  f2_t xi2[3];
+  {
+    int64_t i0 = row0 + 2 * rg, i1 = i0 + 1;
+    if (i0 >= row_end) i0 = row_end - 1;
+    if (i1 >= row_end) i1 = row_end - 1;
+    const float4 a = pk[i0], b = pk[i1];
+    xi2[0] = f2(a.x, b.x); xi2[1] = f2(a.y, b.y); xi2[2] = f2(a.z, b.z);
   }
   int wofs[TPO];
-  uint32_t ahi[TPO];
 #pragma unroll
   for (int k = 0; k < TPO; ++k) {
-    const uint32_t e = tab[og * TPO + k];
-    wofs[k] = srht_w((int)(e & 0xFFFFu), 4 * rq);
-    ahi[k] = e >> 16;
+    const int tt = perm[og * TPO + k];
+    wofs[k] = srht_w(tt >= 0 ? (sel[tt] & (kSrhtB - 1)) : 0, 4 * rq);
   }
-  float acc[TPO][4];
+  f2_t acc[TPO][2];
 #pragma unroll
-  for (int k = 0; k < TPO; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.f;
+  for (int k = 0; k < TPO; ++k) acc[k][0] = acc[k][1] = 0ull;
+  // chunk 0's points
+#pragma unroll
+  for (int q = 0; q < kSrhtB / kSrhtThreads; ++q) cp_async16(Pbuf + t + kSrhtThreads * q, pk + t + kSrhtThreads * q);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
 
   for (int c = 0; c < A; ++c) {
     float* W = Wbuf + (c & 1) * kSrhtSmemFloats;
-    float* wA = W + oA;
-    float* wB = W + oB;
+    if (c + 1 < A) {   // chunk c+1's points into the other tile (its last reader, phase A of c-1, is done)
+      float4* pn = Pbuf + ((c + 1) & 1) * kSrhtB;
+      const float4* src = pk + (int64_t)(c + 1) * kSrhtB;
+#pragma unroll
+      for (int q = 0; q < kSrhtB / kSrhtThreads; ++q) cp_async16(pn + t + kSrhtThreads * q, src + t + kSrhtThreads * q);
+      cp_async_commit();
+    }
     // ---------------- phase A (writes the other buffer than chunk c-1's phase C reads: no barrier before it)
     {
-      const float4* pc = pk + (int64_t)c * kSrhtB + cg;
-      float v[2][16];
+      const float4* pc = Pbuf + (c & 1) * kSrhtB + cg;
+      f2_t v[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const float4 p = __ldg(pc + 32 * q);
-        v[0][q] = cov_signed<DIM, KIND>(xi[0], p);
-        v[1][q] = cov_signed<DIM, KIND>(xi[1], p);
-      }
+      for (int q = 0; q < 16; ++q) v[q] = cov_signed2<DIM, KIND>(xi2, pc[32 * q]);
 #pragma unroll
       for (int h = 1; h < 16; h <<= 1)
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           if (!(q & h)) {
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-              const float x = v[rr][q], y = v[rr][q + h];
-              v[rr][q] = x + y;
-              v[rr][q + h] = x - y;
-            }
+            const f2_t x = v[q], y = v[q + h];
+            v[q] = f2add(x, y);
+            v[q + h] = f2sub(x, y);
           }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) *reinterpret_cast<float2*>(wA + 528 * q) = make_float2(v[0][q], v[1][q]);
+      for (int q = 0; q < 16; ++q) *reinterpret_cast<f2_t*>(W + oA + 264 * q) = v[q];
     }
     __syncthreads();
-    // ---------------- phase B
+    // ---------------- phase B: pairs (b, b+16) packed for l bits 0-3, then bit 4 inside the pairs
     {
-      float u[32];
+      float* wB = W + oB;
+      f2_t u[16];
 #pragma unroll
-      for (int b = 0; b < 32; ++b) u[b] = wB[16 * b];
+      for (int b = 0; b < 16; ++b) u[b] = f2(wB[8 * b], wB[8 * (b + 16)]);
 #pragma unroll
-      for (int h = 1; h < 32; h <<= 1)
+      for (int h = 1; h < 16; h <<= 1)
 #pragma unroll
-        for (int b = 0; b < 32; ++b)
+        for (int b = 0; b < 16; ++b)
           if (!(b & h)) {
-            const float x = u[b], y = u[b + h];
-            u[b] = x + y;
-            u[b + h] = x - y;
+            const f2_t x = u[b], y = u[b + h];
+            u[b] = f2add(x, y);
+            u[b + h] = f2sub(x, y);
           }
 #pragma unroll
-      for (int b = 0; b < 32; ++b) wB[16 * b] = u[b];
+      for (int b = 0; b < 16; ++b) {
+        const float x = f2lo(u[b]), y = f2hi(u[b]);
+        wB[8 * b] = x + y;
+        wB[8 * (b + 16)] = x - y;
+      }
     }
+    cp_async_wait_all();   // chunk c+1's points visible to all threads after the barrier
     __syncthreads();
-    // ---------------- phase C
+    // ---------------- phase C (the chunk's signs are L1-resident: one 4*d_pad-byte row per chunk)
+    float sg[TPO];
+#pragma unroll
+    for (int k = 0; k < TPO; ++k) sg[k] = __ldg(sgn + (int64_t)c * d_pad + og * TPO + k);
 #pragma unroll
     for (int k = 0; k < TPO; ++k) {
-      const float sg = __int_as_float(0x3f800000u | ((__popc((uint32_t)c & ahi[k]) & 1u) << 31));
-      const float4 w = *reinterpret_cast<const float4*>(W + wofs[k]);
-      acc[k][0] = fmaf(sg, w.x, acc[k][0]);
-      acc[k][1] = fmaf(sg, w.y, acc[k][1]);
-      acc[k][2] = fmaf(sg, w.z, acc[k][2]);
-      acc[k][3] = fmaf(sg, w.w, acc[k][3]);
+      const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(W + wofs[k]);
+      acc[k][0] = f2fma(f2s(sg[k]), w.x, acc[k][0]);
+      acc[k][1] = f2fma(f2s(sg[k]), w.y, acc[k][1]);
     }
   }
   // ---------------- epilogue: scale, nugget (by index, reading L9), store.
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const int64_t i = row0 + 4 * rq + rr;
-    if (i >= row_end) continue;
-    const float si = pk[i].w > 0.f ? 1.f : -1.f;
-    float* yrow = Y + (i - row_begin) * (int64_t)d;
+  for (int k = 0; k < TPO; ++k) {
+    const int tt = perm[og * TPO + k];
+    if (tt < 0) continue;
+    const uint32_t S = (uint32_t)sel[tt];
 #pragma unroll
-    for (int k = 0; k < TPO; ++k) {
-      const int tt = og * TPO + k;
-      if (tt < d) {
-        const uint32_t e = tab[tt];
-        const uint32_t S = (e & 0xFFFFu) + (e >> 16) * (uint32_t)kSrhtB;
-        const float h = (__popcll((unsigned long long)i & (unsigned long long)S) & 1) ? -1.f : 1.f;
-        yrow[tt] = fmaf(nugget * si, h * out_scale, acc[k][rr] * out_scale);
-      }
+    for (int rr = 0; rr < 4; ++rr) {
+      const int64_t i = row0 + 4 * rq + rr;
+      if (i >= row_end) continue;
+      const float si = pk[i].w > 0.f ? 1.f : -1.f;
+      const float h = (__popcll((unsigned long long)i & (unsigned long long)S) & 1) ? -1.f : 1.f;
+      const f2_t a2 = acc[k][rr >> 1];
+      const float a = (rr & 1) ? f2hi(a2) : f2lo(a2);
+      Y[(i - row_begin) * (int64_t)d + tt] = fmaf(nugget * si, h * out_scale, a * out_scale);
     }
   }
 }
 
-template <int DIM, int KIND, int TPG>
+template <int DIM, int KIND, int TPO>
 static ks_status launch_srht(const SketchLayout& L, const ks_sketch_desc& D, int64_t rb, int64_t re, float* Y,
                              char* ws, cudaStream_t st) {
-  auto kern = k_sketch_srht<DIM, KIND, TPG>;
-  const int smem = 2 * kSrhtSmemFloats * (int)sizeof(float);
+  auto kern = k_sketch_srht<DIM, KIND, TPO>;
+  const int smem = kSrhtSmemBytes;
   KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = (unsigned)((re - rb + kSrhtRows - 1) / kSrhtRows);
-  kern<<<grid, 256, smem, st>>>(reinterpret_cast<const float4*>(ws + L.off_pk),
-                                reinterpret_cast<const uint32_t*>(ws + L.off_tab), rb, re, L.A, D.d,
+  kern<<<grid, kSrhtThreads, smem, st>>>(reinterpret_cast<const float4*>(ws + L.off_pk),
+                                reinterpret_cast<const int32_t*>(ws + L.off_sel),
+                                reinterpret_cast<const int32_t*>(ws + L.off_perm),
+                                reinterpret_cast<const float*>(ws + L.off_sgn), rb, re, L.A, D.d, L.d_pad,
                                 (float)(1.0 / std::sqrt((double)L.N)), D.nugget, Y);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }
 
 template <int DIM, int KIND>
-static ks_status dispatch_tpg(const SketchLayout& L, const ks_sketch_desc& D, int64_t rb, int64_t re, float* Y,
+static ks_status dispatch_tpo(const SketchLayout& L, const ks_sketch_desc& D, int64_t rb, int64_t re, float* Y,
                               char* ws, cudaStream_t st) {
-  switch (L.tpg) {
+  switch (L.tpo) {
+    case 1: return launch_srht<DIM, KIND, 1>(L, D, rb, re, Y, ws, st);
     case 2: return launch_srht<DIM, KIND, 2>(L, D, rb, re, Y, ws, st);
     case 4: return launch_srht<DIM, KIND, 4>(L, D, rb, re, Y, ws, st);
     case 8: return launch_srht<DIM, KIND, 8>(L, D, rb, re, Y, ws, st);
-    case 16: return launch_srht<DIM, KIND, 16>(L, D, rb, re, Y, ws, st);
   }
   return fail(KS_ERR_UNSUPPORTED, "unsupported SRHT output width");
 }
@@ -399,12 +509,12 @@ ks_status sketch_run(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb,
   if (D.omega == KS_OMEGA_GAUSS) return gauss_sketch_run(D, L, rb, re, Y, ws, st);
   const bool se = D.kernel == KS_KERNEL_SQEXP;
   switch (D.dim) {
-    case 1: return se ? dispatch_tpg<1, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)
-                      : dispatch_tpg<1, KS_KERNEL_MATERN32>(L, D, rb, re, Y, ws, st);
-    case 2: return se ? dispatch_tpg<2, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)
-                      : dispatch_tpg<2, KS_KERNEL_MATERN32>(L, D, rb, re, Y, ws, st);
-    case 3: return se ? dispatch_tpg<3, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)
-                      : dispatch_tpg<3, KS_KERNEL_MATERN32>(L, D, rb, re, Y, ws, st);
+    case 1: return se ? dispatch_tpo<1, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)
+                      : dispatch_tpo<1, KS_KERNEL_MATERN32>(L, D, rb, re, Y, ws, st);
+    case 2: return se ? dispatch_tpo<2, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)
+                      : dispatch_tpo<2, KS_KERNEL_MATERN32>(L, D, rb, re, Y, ws, st);
+    case 3: return se ? dispatch_tpo<3, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)
+                      : dispatch_tpo<3, KS_KERNEL_MATERN32>(L, D, rb, re, Y, ws, st);
   }
   return fail(KS_ERR_INVALID_ARGUMENT, "dim");
 }

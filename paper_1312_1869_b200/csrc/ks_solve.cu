@@ -1,7 +1,7 @@
 // ks_solve.cu -- the low-rank solve after TSQR (readings L11, L14).
 //
 //   C = Q^T A          k_qtx_partial + k_qtx_reduce (deterministic split-K over row chunks)
-//   Z = R^{-1} C       k_trsolve: truncated back substitution, fp64, one CTA
+//   Z = R^{-1} C       k_trsolve: truncated back substitution, fp64, blocked, one CTA per 4 columns
 //   X = Omega Z        ks_sketch.cu (omega_apply_run)
 #include "ks_common.cuh"
 #include "ks_internal.h"
@@ -96,71 +96,109 @@ __global__ void __launch_bounds__(256) k_qc(const float* __restrict__ Q, int64_t
     }
 }
 
-// Truncated back substitution in fp64 (one CTA of 1024 threads).
+// Truncated back substitution in fp64 ("backward substitution"; readings L11, L14).
 //   k = largest prefix with |r_jj| >= tau max|r_ii| (tau > 0), or k = d (tau == 0; a diagonal
 //   <= 1e-12 max|r_ii| is reported as -(index+1) in *kout).
-// Thread t owns column col = t % m and rows j = slot + nslots*q of C (in registers, fp64).
-constexpr int kTrQ = 32;
-__global__ void __launch_bounds__(1024) k_trsolve(const float* __restrict__ R, const float* __restrict__ C, int d,
-                                                  int m, float tau, float* __restrict__ Z, int32_t* __restrict__ kout) {
-  __shared__ double zrow[2][64];
-  __shared__ int s_k;
-  const int tid = threadIdx.x;
-  if (tid < 32) {
-    double mx = 0.0;
-    for (int i = tid; i < d; i += 32) mx = fmax(mx, fabs((double)R[(int64_t)i * d + i]));
-    for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (tid == 0) {
-      int k = 0;
-      if (tau > 0.f) {
-        while (k < d) {
-          const double r = fabs((double)R[(int64_t)k * d + k]);
-          if (!(r >= (double)tau * mx) || r == 0.0) break;
-          ++k;
-        }
-      } else {
-        k = d;
-        for (int i = 0; i < d; ++i)
-          if (fabs((double)R[(int64_t)i * d + i]) <= 1e-12 * mx) { k = -(i + 1); break; }
-      }
-      s_k = k;
-      if (kout) *kout = k;
-    }
+// Blocked right-looking: CTA b owns columns [kTrMC*b, kTrMC*b + kTrMC) of C (fp64 in shared memory).
+// For each 32-row block of R from the bottom: warp 0 solves the 32 x 32 diagonal block (lane = row, its
+// R segment and 1/r_ll in registers), the block's column panel R[0:b0, b0:b0+32) is staged in shared
+// memory by coalesced row reads, and every thread subtracts R[j, block] z[block] from its rows j < b0.
+// Every CTA computes k itself.
+constexpr int kTrMC = 4;
+constexpr int kTrMaxD = 1024;
+constexpr int kTrSmem = kTrMaxD * kTrMC * 8 + kTrMaxD * 33 * 4;   // C block (fp64) + R column panel
+__global__ void __launch_bounds__(256) k_trsolve(const float* __restrict__ R, const float* __restrict__ C, int d,
+                                                 int m, float tau, float* __restrict__ Z, int32_t* __restrict__ kout) {
+  extern __shared__ __align__(16) double trs[];
+  double (*cs)[kTrMC] = reinterpret_cast<double (*)[kTrMC]>(trs);              // [kTrMaxD][kTrMC]
+  float* Rp = reinterpret_cast<float*>(trs + kTrMaxD * kTrMC);                  // [kTrMaxD][33]
+  __shared__ double zb[32][kTrMC];
+  __shared__ float red[8];
+  __shared__ int redi[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col0 = blockIdx.x * kTrMC;
+  const int nc = min(kTrMC, m - col0);
+  // ---- k (parallel max of |r_ii|, then the first failing index)
+  float mx = 0.f;
+  for (int i = tid; i < d; i += 256) mx = fmaxf(mx, fabsf(R[(int64_t)i * d + i]));
+  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int g = 1; g < 8; ++g) mx = fmaxf(mx, red[g]);
+  int first = d;
+  for (int i = tid; i < d; i += 256) {
+    const double r = fabs((double)R[(int64_t)i * d + i]);
+    const bool bad = tau > 0.f ? (!(r >= (double)tau * (double)mx) || r == 0.0) : (r <= 1e-12 * (double)mx);
+    if (bad && i < first) first = i;
   }
+  for (int o = 16; o >= 1; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  if (lane == 0) redi[warp] = first;
   __syncthreads();
-  const int k = s_k;
-  const int nslots = 1024 / m;
-  const int col = tid % m, slot = tid / m;
-  const bool active = slot < nslots;
-  for (int p = tid; p < d * m; p += 1024) Z[p] = 0.f;   // rows >= k stay 0
-  __syncthreads();
+  first = redi[0];
+  for (int g = 1; g < 8; ++g) first = min(first, redi[g]);
+  const int k = tau > 0.f ? first : (first < d ? -(first + 1) : d);
+  if (blockIdx.x == 0 && tid == 0 && kout) *kout = k;
+  for (int p = tid; p < d * nc; p += 256) {
+    const int j = p / nc, c = p - j * nc;
+    Z[(int64_t)j * m + col0 + c] = 0.f;   // rows >= k stay 0
+  }
   if (k <= 0) return;
-  double c[kTrQ];
-#pragma unroll
-  for (int q = 0; q < kTrQ; ++q) {
-    const int j = slot + nslots * q;
-    c[q] = (active && j < k) ? (double)C[(int64_t)j * m + col] : 0.0;
+  for (int p = tid; p < k * kTrMC; p += 256) {
+    const int j = p / kTrMC, c = p - j * kTrMC;
+    cs[j][c] = c < nc ? (double)C[(int64_t)j * m + col0 + c] : 0.0;
   }
-  for (int i = k - 1; i >= 0; --i) {
-    const int par = i & 1;
-    if (active && (i % nslots) == slot) {
-      double ci = 0.0;
+  __syncthreads();
+  for (int b0 = ((k - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
+    const int bw = min(32, k - b0);
+    // stage R[0:b0, b0:b0+bw) (coalesced: a warp reads 32 consecutive floats of a row)
+    for (int j = warp; j < b0; j += 8) Rp[j * 33 + lane] = lane < bw ? R[(int64_t)j * d + b0 + lane] : 0.f;
+    if (warp == 0) {
+      // lane l = row b0 + l: its R segment R[b0+l][b0 .. b0+bw) in registers
+      double rr[32];
+      const float* Rr = R + (int64_t)(b0 + min(lane, bw - 1)) * d + b0;
 #pragma unroll
-      for (int q = 0; q < kTrQ; ++q)
-        if (slot + nslots * q == i) ci = c[q];
-      const double z = ci / (double)R[(int64_t)i * d + i];
-      zrow[par][col] = z;
-      Z[(int64_t)i * m + col] = (float)z;
+      for (int q = 0; q < 32; ++q) rr[q] = (q < bw && lane < bw) ? (double)Rr[q] : 0.0;
+      double inv = 1.0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q == lane) inv = lane < bw ? 1.0 / rr[q] : 0.0;
+      double c[kTrMC];
+#pragma unroll
+      for (int cc = 0; cc < kTrMC; ++cc) c[cc] = lane < bw ? cs[b0 + lane][cc] : 0.0;
+#pragma unroll
+      for (int q = 31; q >= 0; --q) {
+        if (q < bw) {
+#pragma unroll
+          for (int cc = 0; cc < kTrMC; ++cc) {
+            const double zq = __shfl_sync(0xffffffffu, c[cc] * inv, q);   // lane q's value is z_q
+            if (lane == q) c[cc] = zq;
+            else if (lane < q) c[cc] = fma(-rr[q], zq, c[cc]);
+          }
+        }
+      }
+      if (lane < bw) {
+#pragma unroll
+        for (int cc = 0; cc < kTrMC; ++cc) {
+          zb[lane][cc] = c[cc];
+          if (cc < nc) Z[(int64_t)(b0 + lane) * m + col0 + cc] = (float)c[cc];
+        }
+      }
     }
     __syncthreads();
-    if (active) {
-      const double z = zrow[par][col];
+    for (int j = tid; j < b0; j += 256) {
+      double acc[kTrMC];
 #pragma unroll
-      for (int q = 0; q < kTrQ; ++q) {
-        const int j = slot + nslots * q;
-        if (j < i) c[q] = fma(-(double)R[(int64_t)j * d + i], z, c[q]);
+      for (int cc = 0; cc < kTrMC; ++cc) acc[cc] = cs[j][cc];
+      for (int q = 0; q < bw; ++q) {
+        const double r = (double)Rp[j * 33 + q];
+#pragma unroll
+        for (int cc = 0; cc < kTrMC; ++cc) acc[cc] = fma(-r, zb[q][cc], acc[cc]);
       }
+#pragma unroll
+      for (int cc = 0; cc < kTrMC; ++cc) cs[j][cc] = acc[cc];
     }
+    __syncthreads();
   }
 }
 
@@ -188,7 +226,13 @@ ks_status apply_q_run(const float* Q, int64_t rows, int d, const float* C, int m
 }
 
 ks_status trsolve_run(const float* R, const float* C, int d, int m, float tau, float* Z, int32_t* k, cudaStream_t st) {
-  k_trsolve<<<1, 1024, 0, st>>>(R, C, d, m, tau, Z, k);
+  if (d > kTrMaxD) return fail(KS_ERR_UNSUPPORTED, "trsolve supports d <= 1024");
+  static bool attr = false;
+  if (!attr) {
+    KS_CUDA_TRY(cudaFuncSetAttribute(k_trsolve, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrSmem));
+    attr = true;
+  }
+  k_trsolve<<<(unsigned)((m + kTrMC - 1) / kTrMC), 256, kTrSmem, st>>>(R, C, d, m, tau, Z, k);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }
