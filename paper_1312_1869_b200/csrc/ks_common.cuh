@@ -99,6 +99,24 @@ KS_DEVINL f2_t f2fma(f2_t a, f2_t b, f2_t c) {
   return r;
 }
 
+// kappa(r_i0j) and kappa(r_i1j) without the amplitude (SE 2^(-r'^2); Matern-3/2 (1 + z) e^-z): the caller
+// folds the amplitude p.w into its first butterfly level.
+template <int DIM, int KIND>
+KS_DEVINL f2_t cov_kappa2(const f2_t (&xi2)[3], const float4 p) {
+  const f2_t dx = f2sub(xi2[0], f2s(p.x));
+  f2_t r2 = f2mul(dx, dx);
+  if (DIM > 1) { const f2_t dy = f2sub(xi2[1], f2s(p.y)); r2 = f2fma(dy, dy, r2); }
+  if (DIM > 2) { const f2_t dz = f2sub(xi2[2], f2s(p.z)); r2 = f2fma(dz, dz, r2); }
+  if (KIND == KS_KERNEL_SQEXP) {
+    return f2(ex2_approx(-f2lo(r2)), ex2_approx(-f2hi(r2)));
+  } else {
+    const f2_t z = f2(sqrt_approx(f2lo(r2)), sqrt_approx(f2hi(r2)));
+    const f2_t tz = f2mul(z, f2s(-1.4426950408889634f));
+    const f2_t e = f2(ex2_approx(f2lo(tz)), ex2_approx(f2hi(tz)));
+    return f2fma(z, e, e);
+  }
+}
+
 // K[i0,j] s_j and K[i1,j] s_j for a row pair (packed coordinates xi2[c] = (x_i0c, x_i1c)) and one
 // packed point p = (scaled coords, amplitude); same arithmetic as cov_signed, per half.
 template <int DIM, int KIND>

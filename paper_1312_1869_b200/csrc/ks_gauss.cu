@@ -163,11 +163,18 @@ KS_DEVINL void cluster_sync() {
 KS_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-// 1-D bulk copy global -> own shared memory, completing on an mbarrier of this CTA.
-KS_DEVINL void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
+// 2-D tensor copy global -> own shared memory, completing on an mbarrier of this CTA.
+KS_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+KS_DEVINL float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
 }
 KS_DEVINL void tma_load_2d_2cta(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar_cluster) {
   asm volatile(
@@ -192,7 +199,8 @@ KS_DEVINL void umma_commit_2cta(uint32_t bar) {
 
 template <int DIM, int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGThreads, 1)
-k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restrict__ pk, int64_t row_begin,
+k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmP,
+                const float4* __restrict__ pk, int64_t row_begin,
                 int64_t row_end, int nkb, int seg_kb, int DN, float nugget, float out_scale, float* __restrict__ Y) {
   const int kBHalfBytes = (DN / 2) * kGaussBK * 2;
   const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
@@ -201,7 +209,9 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
   uint8_t* a_hi = smem;
   uint8_t* a_lo = smem + kG2Stages * kATileBytes;
   uint8_t* b_t = a_lo + kG2Stages * kATileBytes;
-  float4* pring = reinterpret_cast<float4*>(b_t + kG2Stages * kBHalfBytes);     // [kPtsStages][64] points
+  // [kPtsStages][8 groups][8 points]: TMA SWIZZLE_128B stores point 8g + q of a stage at 16-B chunk q ^ g of
+  // its 128-B row g, so the 8 lanes reading 8 different groups at the same q hit 8 different bank groups.
+  float4* pring = reinterpret_cast<float4*>(b_t + kG2Stages * kBHalfBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(pring + kPtsStages * kGaussBK);
   // full[S], empty[S], accf[2], acce[2], pfull[PS], pempty[PS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kG2Stages + 4 + 2 * kPtsStages);
@@ -230,6 +240,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -258,7 +269,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
         const uint32_t ph = (kb / kPtsStages) & 1;
         mbar_wait(pempty0 + 8 * s, ph ^ 1);
         mbar_arrive_tx(pfull0 + 8 * s, kPtsBytes);
-        bulk_load(smem_u32(pring + s * kGaussBK), pk + (int64_t)kb * kGaussBK, kPtsBytes, pfull0 + 8 * s);
+        tma_load_2d(smem_u32(pring + s * kGaussBK), &tmP, 0, kb * (kGaussBK / 8), pfull0 + 8 * s);
       }
     }
   } else if (warp == 1) {
@@ -314,7 +325,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const float4* __restric
       mbar_wait(pfull0 + 8 * ps, (kb / kPtsStages) & 1);
       float4 pts[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) pts[q] = pring[ps * kGaussBK + 8 * cq + q];
+      for (int q = 0; q < 8; ++q) pts[q] = lds128(smem_u32(pring + ps * kGaussBK + 8 * cq + (q ^ cq)));
       __syncwarp();
       if (lane == 0) mbar_arrive(pempty0 + 8 * ps);   // release: this warp's reads of the slot are done
       mbar_wait(empty0 + 8 * s, ph ^ 1);
@@ -419,6 +430,14 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  CUtensorMap tmP;   // packed points as rows of 8 float4 (128 B), 8-row boxes, SWIZZLE_128B
+  cuuint64_t pdims[2] = {32, (cuuint64_t)(L.ncols_pad / 8)};
+  cuuint64_t pstrides[1] = {128};
+  cuuint32_t pbox[2] = {32, (cuuint32_t)(kGaussBK / 8)};
+  r = encode(&tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ws + L.off_pk, pdims, pstrides, pbox, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled (points) failed: " + std::to_string((int)r));
   const int nkb = (int)(L.ncols_pad / kGaussBK);
   const double S = gauss_scale(D);
   const float nug = (float)(S * D.nugget), osc = (float)(1.0 / (S * std::sqrt((double)D.d)));
@@ -427,7 +446,7 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   auto kern = k_sketch_gauss2<DIM, KIND>;
   KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = 2u * (unsigned)((re - rb + 255) / 256);
-  kern<<<grid, kGThreads, smem, st>>>(tm2, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
+  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }

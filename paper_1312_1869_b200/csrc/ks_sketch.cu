@@ -334,7 +334,8 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
 // Shared tile W: column l (0..511) of the chunk holds its 8 row values at
 // A(l, r) = l*8 + (l >> 5)*8 + r (the (l >> 5) pad makes phase B conflict-free).
 //   phase A : thread (rg = t&3, cg = t>>2) evaluates K*s for the row pair 2rg, 2rg+1 (packed f32x2)
-//             at columns l = cg + 32q, q < 16, butterflies over l bits 5-8 in registers, stores W.
+//             at columns l = cg + 32q, q < 16, butterflies over l bits 5-8 in registers (the first level
+//             with the amplitudes folded into FFMAs), stores W.
 //   phase B : thread (rp = t&7, g = t>>3) loads row rp at l = 32g + b, b < 32, into register pairs
 //             (b, b+16), butterflies over l bits 0-3 (packed) and bit 4, stores back.  W now holds
 //             FWHT_B of the chunk (natural order).
@@ -407,9 +408,15 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
       const float4* pc = Pbuf + (c & 1) * kSrhtB + cg;
       f2_t v[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = cov_signed2<DIM, KIND>(xi2, pc[32 * q]);
+      for (int q = 0; q < 16; q += 2) {   // level h = 1 with the amplitudes a_j = s_j sigma^2 folded in
+        const float4 p0 = pc[32 * q], p1 = pc[32 * (q + 1)];
+        const f2_t k0 = cov_kappa2<DIM, KIND>(xi2, p0), k1 = cov_kappa2<DIM, KIND>(xi2, p1);
+        const f2_t m0 = f2mul(k0, f2s(p0.w));
+        v[q] = f2fma(k1, f2s(p1.w), m0);
+        v[q + 1] = f2fma(k1, f2s(-p1.w), m0);
+      }
 #pragma unroll
-      for (int h = 1; h < 16; h <<= 1)
+      for (int h = 2; h < 16; h <<= 1)
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           if (!(q & h)) {
