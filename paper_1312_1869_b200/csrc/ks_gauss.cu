@@ -43,15 +43,18 @@ KS_DEVINL void mbar_arrive(uint32_t bar) {
 KS_DEVINL void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread sleeps until the phase completes (or the hint
+// expires) instead of re-polling -- the single-lane TMA / MMA / loader roles otherwise spend issue slots
+// of their SMSP spinning (measured: 24 % of the kernel's issued instructions were SYNCS/YIELD polling).
 KS_DEVINL void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(0x989680u)
         : "memory");
   }
 }
@@ -68,6 +71,9 @@ KS_DEVINL uint64_t umma_desc_sw128(uint32_t saddr) {
 }
 
 
+KS_DEVINL void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 KS_DEVINL uint32_t pack_half2(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
@@ -126,8 +132,8 @@ KS_DEVINL void produce_tile(const f2_t (&xi2)[2][3], const int64_t (&irow)[4], c
     for (int h = 0; h < 2; ++h) {
       const int r = 4 * rq + 2 * pr + h;
       const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
-      *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(hi[h][0], hi[h][1], hi[h][2], hi[h][3]);
-      *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[h][0], lo[h][1], lo[h][2], lo[h][3]);
+      sts128(smem_u32(a_hi + off), hi[h][0], hi[h][1], hi[h][2], hi[h][3]);   // st.shared: the tile pointers
+      sts128(smem_u32(a_lo + off), lo[h][0], lo[h][1], lo[h][2], lo[h][3]);   // are generic (aligned base)
     }
   }
 }
@@ -156,12 +162,6 @@ KS_DEVINL uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
 }
 KS_DEVINL void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Remote arrive on the leader's barrier.  Default (.release.cta) semantics, as CUTLASS's ClusterBarrier: the
-// .release.cluster form costs a MEMBAR.ALL.GPU per arrive, and the producers' smem writes reach the
-// leader's MMA through fence.proxy.async + the barrier (waited on by the MMA thread), not through L1.
-KS_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-D tensor copy global -> own shared memory, completing on an mbarrier of this CTA.
 KS_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
@@ -213,8 +213,8 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
   // its 128-B row g, so the 8 lanes reading 8 different groups at the same q hit 8 different bank groups.
   float4* pring = reinterpret_cast<float4*>(b_t + kG2Stages * kBHalfBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(pring + kPtsStages * kGaussBK);
-  // full[S], empty[S], accf[2], acce[2], pfull[PS], pempty[PS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kG2Stages + 4 + 2 * kPtsStages);
+  // full[S], empty[S], accf[2], acce[2], pfull[PS], pempty[PS], lfull[S]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kG2Stages + 4 + 2 * kPtsStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -222,12 +222,14 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kG2Stages);
   const uint32_t accf0 = smem_u32(bars + 2 * kG2Stages), acce0 = smem_u32(bars + 2 * kG2Stages + 2);
   const uint32_t pfull0 = smem_u32(bars + 2 * kG2Stages + 4), pempty0 = pfull0 + 8 * kPtsStages;
+  const uint32_t lfull0 = pempty0 + 8 * kPtsStages;
   const uint32_t full0_L = mapa_u32(full0, 0), acce0_L = mapa_u32(acce0, 0);   // the leader's barriers
   const int nseg = (nkb + seg_kb - 1) / seg_kb;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kG2Stages; ++s) {
-      mbar_init(full0 + 8 * s, 16 + 1);   // 8 producer warps x 2 CTAs + the leader's expect_tx
+      mbar_init(full0 + 8 * s, 8 + 1 + 1);   // leader's 8 producer warps + the peer's relay + expect_tx
+      mbar_init(lfull0 + 8 * s, 8);           // peer: its 8 producer warps (relayed to the leader)
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -260,6 +262,17 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
         mbar_wait(empty0 + 8 * s, ph ^ 1);
         if (rank == 0) mbar_arrive_tx(full0 + 8 * s, 2 * kBHalfBytes);
         tma_load_2d_2cta(smem_u32(b_t + s * kBHalfBytes), &tmB, kb * kGaussBK, (int)rank * (DN / 2), full0_L + 8 * s);
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------- peer relay: the peer's A tiles are written by generic stores and read by the leader's
+    // MMA; a release at CLUSTER scope is needed for that (a CTA-scope arrive is not enough).  One thread
+    // collects the 8 producer warps on a local barrier and issues one cluster-scope arrive per stage.
+    if (rank == 1 && lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kG2Stages;
+        mbar_wait(lfull0 + 8 * s, (kb / kG2Stages) & 1);
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(full0_L + 8 * s) : "memory");
       }
     }
   } else if (warp == 2) {
@@ -333,7 +346,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       produce_tile<DIM, KIND>(xi2, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(full0_L + 8 * s);
+      if (lane == 0) mbar_arrive(rank == 0 ? full0 + 8 * s : lfull0 + 8 * s);
     }
   } else if (warp >= 12) {
     // ---------------- drainers: Y[row, :] (+)= acc[g & 1][row, :] in fp32, scaled after the last segment
@@ -379,7 +392,10 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acce0_L + 8 * buf);
+      if (lane == 0) {   // once per segment: cluster-scope release (this CTA's TMEM reads -> the leader's MMA)
+        if (rank == 0) mbar_arrive(acce0 + 8 * buf);
+        else asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce0_L + 8 * buf) : "memory");
+      }
     }
   }
   tc_fence_before();
