@@ -14,8 +14,8 @@
 // operands, so the operand error is the <= 2^-21 relative split error of K.
 // The tensor core's fp32 accumulation is not round-to-nearest (its error grows
 // linearly with the number of MMAs accumulated: tools/gauss_precision.py), so
-// the column loop is cut into segments whose partial sums are drained from TMEM
-// (double buffered) and added to Y in fp32 by dedicated warps.
+// the column loop is cut into segments whose partial sums are folded by dedicated warps into a running
+// sum kept in the other half of TMEM, with fp32 round-to-nearest adds.
 //
 #include "ks_common.cuh"
 #include "ks_internal.h"
@@ -79,6 +79,14 @@ KS_DEVINL uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+KS_DEVINL void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
 KS_DEVINL void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -201,7 +209,8 @@ template <int DIM, int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGThreads, 1)
 k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmP,
                 const float4* __restrict__ pk, int64_t row_begin,
-                int64_t row_end, int nkb, int seg_kb, int DN, float nugget, float out_scale, float* __restrict__ Y) {
+                int64_t row_end, int nkb, int seg_kb, int DN, float nugget, float out_scale, float* __restrict__ Y,
+                int dbg) {
   const int kBHalfBytes = (DN / 2) * kGaussBK * 2;
   const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
@@ -289,10 +298,9 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
     if (rank == 0 && lane == 0) {  // ---------------- MMA issuer (leader only)
       const uint32_t idesc = (1u << 4) | ((uint32_t)(DN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
       for (int g = 0; g < nseg; ++g) {
-        const int buf = g & 1;
-        mbar_wait(acce0 + 8 * buf, ((g >> 1) & 1) ^ 1);
+        mbar_wait(acce0, (g & 1) ^ 1);   // the drainers have folded segment g-1 into the running sum
         tc_fence_after();
-        const uint32_t dtm = tmem + (uint32_t)(buf * DN);
+        const uint32_t dtm = tmem;
         const int kb1 = min(nkb, (g + 1) * seg_kb);
         for (int kb = g * seg_kb; kb < kb1; ++kb) {
           const int s = kb % kG2Stages;
@@ -304,12 +312,14 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
           const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBHalfBytes));
 #pragma unroll
           for (int kk = 0; kk < kGaussBK / 16; ++kk) {
-            umma_f16_2cta(dtm, dh + 2 * kk, db + 2 * kk, idesc, (kb != g * seg_kb || kk != 0) ? 1u : 0u);
-            umma_f16_2cta(dtm, dl + 2 * kk, db + 2 * kk, idesc, 1u);
+            if (!(dbg & 1)) {   // timing studies only (KS_GAUSS_DEBUG): bit 0 skips the MMAs
+              umma_f16_2cta(dtm, dh + 2 * kk, db + 2 * kk, idesc, (kb != g * seg_kb || kk != 0) ? 1u : 0u);
+              umma_f16_2cta(dtm, dl + 2 * kk, db + 2 * kk, idesc, 1u);
+            }
           }
           umma_commit_2cta(empty0 + 8 * s);
         }
-        umma_commit_2cta(accf0 + 8 * buf);
+        umma_commit_2cta(accf0);
       }
     }
   } else if (warp >= 4 && warp < 12) {
@@ -343,13 +353,15 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       if (lane == 0) mbar_arrive(pempty0 + 8 * ps);   // release: this warp's reads of the slot are done
       mbar_wait(empty0 + 8 * s, ph ^ 1);
       const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
-      produce_tile<DIM, KIND>(xi2, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
+      if (!(dbg & 2))   // bit 1 skips the producers' arithmetic
+        produce_tile<DIM, KIND>(xi2, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(rank == 0 ? full0 + 8 * s : lfull0 + 8 * s);
     }
   } else if (warp >= 12) {
-    // ---------------- drainers: Y[row, :] (+)= acc[g & 1][row, :] in fp32, scaled after the last segment
+    // ---------------- drainers: running sum (TMEM columns [DN, 2 DN)) += segment accumulator (columns
+    // [0, DN)), added in fp32 round-to-nearest on the CUDA cores; the last segment is scaled and stored.
     const int quarter = warp & 3;
     const int row = 32 * quarter + lane;
     const int64_t i = row0 + row;
@@ -357,44 +369,36 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
     float* yr = Y + (i - row_begin) * (int64_t)DN;
     const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
     for (int g = 0; g < nseg; ++g) {
-      const int buf = g & 1;
-      mbar_wait(accf0 + 8 * buf, (g >> 1) & 1);
+      mbar_wait(accf0, g & 1);
       tc_fence_after();
       const bool first = g == 0, last = g == nseg - 1;
-      for (int c0 = 0; c0 < DN; c0 += 64) {   // 64 columns per batch: all of Y's loads in flight together
-        const int nb = min(64, DN - c0);
-        float4 o[16];
-        if (ok && !first) {
+      for (int c0 = 0; c0 < DN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + (uint32_t)c0, v);
+        if (!first) {
+          float u[16];
+          tmem_ld16(tl + (uint32_t)(DN + c0), u);
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (4 * q < nb) o[q] = reinterpret_cast<const float4*>(yr + c0)[q];
+          for (int q = 0; q < 16; ++q) v[q] += u[q];
         }
+        if (last) {
+          if (ok) {
+            float4* dst = reinterpret_cast<float4*>(yr + c0);
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          if (16 * h < nb) {
-            float v[16];
-            tmem_ld16(tl + (uint32_t)(buf * DN + c0 + 16 * h), v);
-            if (ok) {
-              float4* dst = reinterpret_cast<float4*>(yr + c0 + 16 * h);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                if (!first) {
-                  const float4 y = o[4 * h + q];
-                  x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
-                }
-                if (last) { x.x *= out_scale; x.y *= out_scale; x.z *= out_scale; x.w *= out_scale; }
-                dst[q] = x;
-              }
-            }
+            for (int q = 0; q < 4; ++q)
+              dst[q] = make_float4(v[4 * q] * out_scale, v[4 * q + 1] * out_scale, v[4 * q + 2] * out_scale,
+                                   v[4 * q + 3] * out_scale);
           }
+        } else {
+          tmem_st16(tl + (uint32_t)(DN + c0), v);
         }
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {   // once per segment: cluster-scope release (this CTA's TMEM reads -> the leader's MMA)
-        if (rank == 0) mbar_arrive(acce0 + 8 * buf);
-        else asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce0_L + 8 * buf) : "memory");
+      if (lane == 0) {   // once per segment: cluster-scope release (this CTA's TMEM accesses -> the leader's MMA)
+        if (rank == 0) mbar_arrive(acce0);
+        else asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce0_L) : "memory");
       }
     }
   }
@@ -462,7 +466,8 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   auto kern = k_sketch_gauss2<DIM, KIND>;
   KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned grid = 2u * (unsigned)((re - rb + 255) / 256);
-  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y);
+  static const int dbg = [] { const char* e = getenv("KS_GAUSS_DEBUG"); return e ? atoi(e) : 0; }();
+  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y, dbg);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }
