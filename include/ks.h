@@ -121,11 +121,19 @@ KS_API ks_status ks_omega_apply(const ks_sketch_desc* desc, const float* Z_dev, 
  * Limits: 1 <= d <= 512, every block must have >= d rows. */
 typedef struct ks_tsqr_plan* ks_tsqr_handle;
 
-KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks, size_t* bytes);
+/* Merge topology of the block R's: the pairwise tree (eqs. (2)-(3), the default) or the chain of
+ * eq. (5) (the running R absorbs one block R per step).  R is the same (unique). */
+typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1 } ks_tsqr_topology;
 
-/* Create a plan over a caller-owned device workspace (kept until destroy). */
+KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks, size_t* bytes);
+KS_API ks_status ks_tsqr_workspace_size_ex(int64_t rows, int32_t d, int32_t blocks, int32_t topology, size_t* bytes);
+
+/* Create a plan over a caller-owned device workspace (kept until destroy).  _ex selects the topology
+ * (KS_ERR_INVALID_ARGUMENT for an unknown one). */
 KS_API ks_status ks_tsqr_create(int64_t rows, int32_t d, int32_t blocks, void* ws_dev, size_t ws_bytes,
                          ks_tsqr_handle* out);
+KS_API ks_status ks_tsqr_create_ex(int64_t rows, int32_t d, int32_t blocks, int32_t topology, void* ws_dev,
+                            size_t ws_bytes, ks_tsqr_handle* out);
 KS_API ks_status ks_tsqr_destroy(ks_tsqr_handle h);
 
 /* Factor Y (device, rows x d, not modified).  R_dev: d x d output.  If Q_dev is
@@ -136,6 +144,16 @@ KS_API ks_status ks_tsqr(ks_tsqr_handle h, const float* Y_dev, float* Q_dev, flo
 /* Q_dev (rows x d) = Q-hat * C, with C (d x d, device) or C = I if C_dev == NULL.
  * Multi-GPU second level: C = this rank's d x d block of the merge's Q2. */
 KS_API ks_status ks_qform(ks_tsqr_handle h, const float* C_dev, float* Q_dev, ks_stream_t stream);
+
+/* Implicit Q ("the matrix product for forming Q-hat need not be evaluated at all"),
+ * valid after ks_tsqr on the handle; the stored reflectors are applied directly (4 rows d m flops
+ * instead of forming Q):
+ *   ks_tsqr_apply_qt: C_dev (d x m) = Q-hat^T X.  X_dev (rows x m, device) is overwritten (it holds
+ *                     Q_full^T X on return; C is its first d rows).
+ *   ks_tsqr_apply_q : X_dev (rows x m) = Q-hat C, C_dev d x m.
+ * m >= 1; row-major fp32; stream-ordered. */
+KS_API ks_status ks_tsqr_apply_qt(ks_tsqr_handle h, float* X_dev, int32_t m, float* C_dev, ks_stream_t stream);
+KS_API ks_status ks_tsqr_apply_q(ks_tsqr_handle h, const float* C_dev, int32_t m, float* X_dev, ks_stream_t stream);
 
 /* Second TSQR level (eq. (5)'s final merge of per-unit R's):
  * QR of the stacked (P*d) x d matrix of per-rank R's.  Q2_dev: (P*d) x d

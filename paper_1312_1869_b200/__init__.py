@@ -20,7 +20,8 @@ import torch
 __all__ = [
     "KsError", "SketchDesc", "SQEXP", "MATERN32", "SRHT", "GAUSS", "lib", "library_path",
     "ks_sketch_workspace_size", "ks_sketch", "ks_omega_export", "ks_omega_apply",
-    "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr", "ks_qform",
+    "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr", "ks_qform", "TSQR_TREE", "TSQR_CHAIN",
+    "ks_tsqr_workspace_size_ex", "ks_tsqr_create_ex", "ks_tsqr_apply_qt", "ks_tsqr_apply_q",
     "ks_tsqr_merge_workspace_size", "ks_tsqr_merge", "ks_apply_qt_workspace_size", "ks_apply_qt",
     "ks_apply_q", "ks_trsolve", "ks_lowrank_workspace_size", "ks_lowrank_solve", "ks_last_error",
     "ks_version", "Sketch", "TsqrPlan", "Pipeline", "make_desc",
@@ -61,6 +62,10 @@ _SIGS = {
     "ks_omega_apply": [C.POINTER(SketchDesc), _P, _i32, _i64, _i64, _P, _P, _sz, _P],
     "ks_tsqr_workspace_size": [_i64, _i32, _i32, C.POINTER(_sz)],
     "ks_tsqr_create": [_i64, _i32, _i32, _P, _sz, C.POINTER(_P)],
+    "ks_tsqr_workspace_size_ex": [_i64, _i32, _i32, _i32, C.POINTER(_sz)],
+    "ks_tsqr_create_ex": [_i64, _i32, _i32, _i32, _P, _sz, C.POINTER(_P)],
+    "ks_tsqr_apply_qt": [_P, _P, _i32, _P, _P],
+    "ks_tsqr_apply_q": [_P, _P, _i32, _P, _P],
     "ks_tsqr_destroy": [_P],
     "ks_tsqr": [_P, _P, _P, _P, _P],
     "ks_qform": [_P, _P, _P, _P],
@@ -169,6 +174,32 @@ def ks_tsqr_create(rows, d, blocks, ws) -> C.c_void_p:
     return h
 
 
+TSQR_TREE, TSQR_CHAIN = 0, 1
+
+
+def ks_tsqr_workspace_size_ex(rows, d, blocks, topology) -> int:
+    b = _sz(0)
+    _check(lib().ks_tsqr_workspace_size_ex(int(rows), int(d), int(blocks), int(topology), C.byref(b)))
+    return b.value
+
+
+def ks_tsqr_create_ex(rows, d, blocks, topology, ws) -> C.c_void_p:
+    h = C.c_void_p()
+    _check(lib().ks_tsqr_create_ex(int(rows), int(d), int(blocks), int(topology), _ptr(ws),
+                                   ws.numel() * ws.element_size(), C.byref(h)))
+    return h
+
+
+def ks_tsqr_apply_qt(h, X, m, Cmat, stream=None):
+    _check(lib().ks_tsqr_apply_qt(h, _ptr(X, torch.float32, "X"), int(m), _ptr(Cmat, torch.float32, "C"),
+                                  _stream(stream)))
+
+
+def ks_tsqr_apply_q(h, Cmat, m, X, stream=None):
+    _check(lib().ks_tsqr_apply_q(h, _ptr(Cmat, torch.float32, "C"), int(m), _ptr(X, torch.float32, "X"),
+                                 _stream(stream)))
+
+
 def ks_tsqr_destroy(h):
     _check(lib().ks_tsqr_destroy(h))
 
@@ -270,10 +301,10 @@ class Sketch:
 class TsqrPlan:
     """Blocked TSQR plan over a torch-owned workspace."""
 
-    def __init__(self, rows, d, blocks, device="cuda"):
+    def __init__(self, rows, d, blocks, device="cuda", topology=TSQR_TREE):
         self.rows, self.d, self.blocks = int(rows), int(d), int(blocks)
-        self.ws = _ws(ks_tsqr_workspace_size(rows, d, blocks), device)
-        self.h = ks_tsqr_create(rows, d, blocks, self.ws)
+        self.ws = _ws(ks_tsqr_workspace_size_ex(rows, d, blocks, topology), device)
+        self.h = ks_tsqr_create_ex(rows, d, blocks, topology, self.ws)
         self.device = torch.device(device)
 
     def __del__(self):
@@ -295,6 +326,20 @@ class TsqrPlan:
             Q = torch.empty((self.rows, self.d), dtype=torch.float32, device=self.device)
         ks_qform(self.h, Cmat, Q, stream)
         return Q
+
+    def apply_qt(self, X, stream=None):
+        """Implicit Q-hat^T X (X rows x m is copied, not modified); returns C (d x m)."""
+        Xw = X.contiguous().clone()
+        Cm = torch.empty((self.d, Xw.shape[1]), dtype=torch.float32, device=self.device)
+        ks_tsqr_apply_qt(self.h, Xw, Xw.shape[1], Cm, stream)
+        return Cm
+
+    def apply_q(self, Cmat, stream=None):
+        """Implicit Q-hat C (C d x m); returns X (rows x m)."""
+        Cmat = Cmat.contiguous()
+        X = torch.empty((self.rows, Cmat.shape[1]), dtype=torch.float32, device=self.device)
+        ks_tsqr_apply_q(self.h, Cmat, Cmat.shape[1], X, stream)
+        return X
 
 
 class Pipeline:

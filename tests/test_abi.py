@@ -63,6 +63,15 @@ def test_unsupported_sizes_are_reported():
     assert e.value.status == 5
 
 
+def test_tsqr_topology_validation():
+    import paper_1312_1869_b200 as ks
+    chain = ks.ks_tsqr_workspace_size_ex(262144, 512, 8, ks.TSQR_CHAIN)
+    tree = ks.ks_tsqr_workspace_size_ex(262144, 512, 8, ks.TSQR_TREE)
+    assert chain > 262144 * 512 * 4 and tree == ks.ks_tsqr_workspace_size(262144, 512, 8)
+    with pytest.raises(ks.KsError):
+        ks.ks_tsqr_workspace_size_ex(1000, 10, 2, 7)
+
+
 def test_tsqr_workspace_rejects_wide_blocks():
     import paper_1312_1869_b200 as ks
     with pytest.raises(ks.KsError) as e:

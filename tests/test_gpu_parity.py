@@ -99,7 +99,7 @@ def test_sketch_full_config_sampled_rows(ks, cuda, name, nrows):
 
 # ---------------------------------------------------------------- TSQR
 TSQR_CASES = [(2048, 64, 4), (16384, 128, 8), (4096, 256, 16), (8192, 512, 8), (3000, 100, 3), (700, 33, 5),
-              (512, 512, 1)]
+              (512, 512, 1), (530, 512, 1), (40000, 64, 3)]   # (530, 512, 1): one 530-row leaf (512-thread QR)
 
 
 @pytest.mark.parametrize("rows,d,blocks", TSQR_CASES)
@@ -114,6 +114,40 @@ def test_tsqr_random_matrix_matches_oracle(ks, cuda, rows, d, blocks):
     assert relF(R, Rr) <= R_TOL
     assert np.linalg.norm(Q.T @ Q - np.eye(d)) <= 1e-4 * np.sqrt(d)
     assert relF(Q @ R, Y) <= 1e-5
+
+
+@pytest.mark.parametrize("rows,d,blocks", [(4096, 64, 8), (6000, 100, 5), (16384, 128, 16)])
+def test_tsqr_chain_topology_matches_oracle_chain(ks, cuda, rows, d, blocks):
+    """PAPER.md eq. (5) chain topology: R equals the oracle's chain TSQR (and hence the tree's, R unique)."""
+    rng = np.random.default_rng(rows + 7 * d)
+    Y = rng.standard_normal((rows, d)).astype(np.float32)
+    plan = ks.TsqrPlan(rows, d, blocks, cuda, topology=ks.TSQR_CHAIN)
+    Q, R = plan.factor(_t(Y, cuda))
+    Q, R = Q.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
+    Rc = oracle.tsqr_chain(Y.astype(np.float64), blocks)
+    assert np.all(np.tril(R, -1) == 0) and np.all(np.diag(R) >= 0)
+    assert relF(R, Rc) <= R_TOL
+    assert np.linalg.norm(Q.T @ Q - np.eye(d)) <= 1e-4 * np.sqrt(d)
+    assert relF(Q @ R, Y) <= 1e-5
+
+
+@pytest.mark.parametrize("rows,d,blocks,m,topology", [(8192, 128, 8, 16, 0), (4096, 64, 4, 5, 0), (3000, 100, 3, 8, 1),
+                                                       (65536, 256, 16, 32, 0)])
+def test_tsqr_implicit_q_applies(ks, cuda, rows, d, blocks, m, topology):
+    """Implicit Q: Q^T A from the stored reflectors.  Pinned by Y^T A = R^T (Q^T A) in fp64
+    (independent of the explicit Q) and against the explicit Q; Q C likewise."""
+    rng = np.random.default_rng(rows + m)
+    Y = rng.standard_normal((rows, d)).astype(np.float32)
+    A = rng.standard_normal((rows, m)).astype(np.float32)
+    plan = ks.TsqrPlan(rows, d, blocks, cuda, topology=topology)
+    Q, R = plan.factor(_t(Y, cuda))
+    Ci = plan.apply_qt(_t(A, cuda)).cpu().numpy().astype(np.float64)
+    R64, Q64 = R.cpu().numpy().astype(np.float64), Q.cpu().numpy().astype(np.float64)
+    assert relF(R64.T @ Ci, Y.astype(np.float64).T @ A.astype(np.float64)) <= 1e-5
+    assert relF(Ci, Q64.T @ A.astype(np.float64)) <= 1e-5
+    Cm = rng.standard_normal((d, m)).astype(np.float32)
+    Xi = plan.apply_q(_t(Cm, cuda)).cpu().numpy().astype(np.float64)
+    assert relF(Xi, Q64 @ Cm.astype(np.float64)) <= 1e-5
 
 
 @pytest.mark.parametrize("name,over", [("c1", {}), ("c2", {}), ("c3", dict(n=8192, blocks=8)), ("c5", dict(n=8192, blocks=2))])
