@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -209,8 +210,13 @@ template <int DIM, int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGThreads, 1)
 k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmP,
                 const float4* __restrict__ pk, int64_t row_begin,
-                int64_t row_end, int nkb, int seg_kb, int DN, float nugget, float out_scale, float* __restrict__ Y,
-                int dbg) {
+                int64_t row_end, int nkb_all, int seg_kb, int DN, float nugget, float out_scale,
+                float* __restrict__ Y0, float* __restrict__ Y1, int dbg) {
+  // split-K: blockIdx.y selects the half of the column blocks (Y0 gets the first half's partial sum,
+  // Y1 the second's; k_add_halves adds them) so that the row tiles fill a whole number of waves.
+  const int kh = blockIdx.y, nkb_a = gridDim.y > 1 ? nkb_all / 2 : nkb_all;
+  const int kb0 = kh * nkb_a, nkb = kh ? nkb_all - nkb_a : nkb_a;
+  float* __restrict__ Y = kh ? Y1 : Y0;
   const int kBHalfBytes = (DN / 2) * kGaussBK * 2;
   const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
@@ -270,7 +276,8 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
         const uint32_t ph = (kb / kG2Stages) & 1;
         mbar_wait(empty0 + 8 * s, ph ^ 1);
         if (rank == 0) mbar_arrive_tx(full0 + 8 * s, 2 * kBHalfBytes);
-        tma_load_2d_2cta(smem_u32(b_t + s * kBHalfBytes), &tmB, kb * kGaussBK, (int)rank * (DN / 2), full0_L + 8 * s);
+        tma_load_2d_2cta(smem_u32(b_t + s * kBHalfBytes), &tmB, (kb0 + kb) * kGaussBK, (int)rank * (DN / 2),
+                         full0_L + 8 * s);
       }
     }
   } else if (warp == 3) {
@@ -291,7 +298,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
         const uint32_t ph = (kb / kPtsStages) & 1;
         mbar_wait(pempty0 + 8 * s, ph ^ 1);
         mbar_arrive_tx(pfull0 + 8 * s, kPtsBytes);
-        tma_load_2d(smem_u32(pring + s * kGaussBK), &tmP, 0, kb * (kGaussBK / 8), pfull0 + 8 * s);
+        tma_load_2d(smem_u32(pring + s * kGaussBK), &tmP, 0, (kb0 + kb) * (kGaussBK / 8), pfull0 + 8 * s);
       }
     }
   } else if (warp == 1) {
@@ -343,7 +350,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kG2Stages;
       const uint32_t ph = (kb / kG2Stages) & 1;
-      const int64_t j0 = (int64_t)kb * kGaussBK + 8 * cq;
+      const int64_t j0 = (int64_t)(kb0 + kb) * kGaussBK + 8 * cq;
       const int ps = kb % kPtsStages;
       mbar_wait(pfull0 + 8 * ps, (kb / kPtsStages) & 1);
       float4 pts[8];
@@ -410,6 +417,16 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
   }
 }
 
+// Y0 += Y1 (the two split-K partial sums; d % 16 == 0 so rows x d is a multiple of 4).
+__global__ void k_add_halves(float4* __restrict__ Y0, const float4* __restrict__ Y1, int64_t n4) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n4; p += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = Y0[p];
+    const float4 b = Y1[p];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    Y0[p] = a;
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -463,12 +480,28 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   const float nug = (float)(S * D.nugget), osc = (float)(1.0 / (S * std::sqrt((double)D.d)));
   const float4* pk = reinterpret_cast<const float4*>(ws + L.off_pk);
   const int smem = 1024 + kG2Stages * (2 * kATileBytes + (DN / 2) * kGaussBK * 2) + kPtsStages * kPtsBytes + 512;
+  // split the column blocks in two when the row tiles leave a partial last wave (one CTA pair per 2 SMs)
+  static const int pair_slots = [] {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms / 2;
+  }();
+  const int64_t pairs = (re - rb + 255) / 256;
+  const int ksplit = (nkb >= 2 && pairs % pair_slots != 0 && pairs < 16 * pair_slots) ? 2 : 1;
+  float* Y1 = reinterpret_cast<float*>(ws + L.off_ybuf);
   auto kern = k_sketch_gauss2<DIM, KIND>;
   KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const unsigned grid = 2u * (unsigned)((re - rb + 255) / 256);
+  const dim3 grid(2u * (unsigned)pairs, (unsigned)ksplit);
   static const int dbg = [] { const char* e = getenv("KS_GAUSS_DEBUG"); return e ? atoi(e) : 0; }();
-  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y, dbg);
+  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y, Y1, dbg);
   KS_LAUNCH_CHECK();
+  if (ksplit == 2) {
+    const int64_t tot = (re - rb) * (int64_t)DN;
+    k_add_halves<<<(unsigned)std::min<int64_t>((tot / 4 + 255) / 256, 148 * 16), 256, 0, st>>>(
+        reinterpret_cast<float4*>(Y), reinterpret_cast<const float4*>(Y1), tot / 4);
+    KS_LAUNCH_CHECK();
+  }
   return KS_OK;
 }
 

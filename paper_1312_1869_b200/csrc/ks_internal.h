@@ -47,7 +47,7 @@ struct SketchLayout {
   int A;              // number of kSrhtB-chunks covering [0, n) (Omega-apply)
   int tpo;            // SRHT sketch: outputs per thread in the gather phase
   int d_pad;          // SRHT sketch: output slots, 64 * tpo (slot -> output by the perm table)
-  size_t off_pk, off_tab, off_sel, off_bucket_ofs, off_bucket_idx, off_bitmap, off_gauss, off_perm, off_sgn, bytes;
+  size_t off_pk, off_tab, off_sel, off_bucket_ofs, off_bucket_idx, off_bitmap, off_gauss, off_perm, off_sgn, off_ybuf, bytes;
 };
 
 ks_status sketch_validate(const ks_sketch_desc* desc);

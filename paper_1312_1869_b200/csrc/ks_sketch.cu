@@ -54,6 +54,8 @@ SketchLayout sketch_layout(const ks_sketch_desc& desc) {
   L.off_gauss = take(desc.omega == KS_OMEGA_GAUSS ? sizeof(__half) * (size_t)desc.d * (size_t)L.ncols_pad : 0);
   L.off_perm = take(desc.omega == KS_OMEGA_SRHT ? sizeof(int32_t) * (size_t)L.d_pad : 0);
   L.off_sgn = take(desc.omega == KS_OMEGA_SRHT ? sizeof(float) * (size_t)L.A * (size_t)L.d_pad : 0);
+  // Gaussian split-K: the second half's partial Y (rows x d)
+  L.off_ybuf = take(desc.omega == KS_OMEGA_GAUSS ? sizeof(float) * (size_t)desc.n * (size_t)desc.d : 0);
   L.bytes = off;
   return L;
 }
