@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 import ks_inputs  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r1_sketch_traffic.json")   # ncu --set full, per launch
 FALLBACK_SM_MHZ = 1965.0
 
 
@@ -350,6 +351,13 @@ def run_ours(args, cfg, pts_np, A_np):
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": None, "kernel": "k_sketch_gauss",
                     "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst); fp16 dense = bf16 rate"}
+        try:   # DRAM bytes of one launch of this config's sketch kernel from a committed ncu capture
+            tr = json.load(open(TRAFFIC_PATH)).get(args.config) if world == 1 else None
+        except (OSError, ValueError):
+            tr = None
+        if tr:
+            roof["traffic"] = tr["traffic_bytes"]
+            roof["traffic_source"] = f"{os.path.relpath(TRAFFIC_PATH, ROOT)} ({tr['kernel']})"
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             st = OracleStep(cfg, pts_np, A_np, rows_hint=args.cpu_rows)
