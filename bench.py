@@ -349,7 +349,7 @@ def run_ours(args, cfg, pts_np, A_np):
             achieved = flops / (t_sk * 1e-3) / 1e12
             peak = float(peaks.get("bf16_tflops", 1590.0))
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None, "kernel": "k_sketch_gauss",
+                    "frac": achieved / peak, "traffic": None, "kernel": "k_sketch_gauss2",
                     "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst); fp16 dense = bf16 rate"}
         try:   # DRAM bytes of one launch of this config's sketch kernel from a committed ncu capture
             tr = json.load(open(TRAFFIC_PATH)).get(args.config) if world == 1 else None
