@@ -156,7 +156,9 @@ KS_API ks_status ks_tsqr_apply_qt(ks_tsqr_handle h, float* X_dev, int32_t m, flo
 KS_API ks_status ks_tsqr_apply_q(ks_tsqr_handle h, const float* C_dev, int32_t m, float* X_dev, ks_stream_t stream);
 
 /* Second TSQR level (eq. (5)'s final merge of per-unit R's):
- * QR of the stacked (P*d) x d matrix of per-rank R's.  Q2_dev: (P*d) x d
+ * one QR of the stacked (P*d) x d matrix of per-rank R's (a single block: leaves of <= 512 stacked
+ * rows merged by one flat level, not a second binary tree -- the latency of the merge is on every
+ * rank's critical path).  Q2_dev: (P*d) x d
  * explicit, R_dev: d x d.  Run redundantly on every rank. */
 KS_API ks_status ks_tsqr_merge_workspace_size(int32_t P, int32_t d, size_t* bytes);
 KS_API ks_status ks_tsqr_merge(const float* Rstack_dev, int32_t P, int32_t d, float* Q2_dev, float* R_dev, void* ws_dev,

@@ -13,6 +13,7 @@ static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 }  // namespace ks
 
 extern "C" uint64_t ks_launch_count(void) { return ks::g_launches.load(); }
@@ -190,6 +191,7 @@ extern "C" ks_status ks_lowrank_solve(const ks_sketch_desc* desc, const float* p
   KS_TRY(ks_sketch(desc, pts, 0, n, Y, w + L.off_sk, sk, stream));
   ks_tsqr_handle h = nullptr;
   KS_TRY(ks_tsqr_create(n, d, blocks, w + L.off_tsqr, tsqr, &h));
+  tsqr_set_graphs(h, false);   // one-shot plan: capturing a graph would not pay off
   ks_status s = ks_tsqr(h, Y, Q, R, stream);
   ks_tsqr_destroy(h);
   KS_TRY(s);

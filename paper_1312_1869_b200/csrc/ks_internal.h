@@ -21,6 +21,7 @@ inline ks_status fail(ks_status code, const std::string& msg) { set_error(msg); 
   } while (0)
 
 void count_launch();
+void add_launches(uint64_t n);   // kernels of a replayed CUDA graph
 
 // After every <<<...>>> launch: count it (ks_launch_count) and check the launch error.
 #define KS_LAUNCH_CHECK()                \
@@ -66,6 +67,10 @@ ks_status omega_export_run(const ks_sketch_desc& desc, const SketchLayout& L, in
                            uint16_t* gauss, char* ws, cudaStream_t st);
 ks_status gauss_sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, int64_t row_begin,
                            int64_t row_end, float* Y, char* ws, cudaStream_t st);
+
+// ---------------------------------------------------------------- TSQR
+// Plans replay their launch sequence as a cached CUDA graph; one-shot plans switch that off.
+void tsqr_set_graphs(ks_tsqr_handle h, bool on);
 
 // ---------------------------------------------------------------- solve side
 ks_status apply_qt_ws(int64_t rows, int d, int m, size_t* bytes);

@@ -43,7 +43,8 @@ class CudaOps:
         f32 = dict(dtype=torch.float32, device=self.device)
         self.sk = Sketch(self.desc, self.device)
         self.plan = TsqrPlan(rows, d, blocks_per_rank, self.device)
-        self.mplan = TsqrPlan(world * d, d, world, self.device) if world > 1 else None
+        # the second level: one QR of the stacked R's (a single block)
+        self.mplan = TsqrPlan(world * d, d, 1, self.device) if world > 1 else None
         self.Y = torch.empty((rows, d), **f32)
         self.Q = torch.empty((rows, d), **f32)
         self.Rp = torch.empty((d, d), **f32)
