@@ -111,6 +111,8 @@ SQEXP = 0
 MATERN32 = 1
 OMEGA_SRHT = 0
 OMEGA_GAUSS = 1
+OMEGA_DHT = 2     # NEXT-1: structured Omega with the discrete Hartley transform ("HP")
+OMEGA_DCT = 3     # NEXT-1: structured Omega with the discrete cosine transform ("HC")
 
 CONFIGS = {
     "c1": dict(n=2048, dim=1, dist="uniform", kernel=SQEXP, sigma2=1.0, ell=0.1, nugget=1e-6,

@@ -27,6 +27,7 @@ _SRC = os.path.join(_HERE, "ks_oracle.c")
 _LIB = os.path.join(_HERE, "libks_oracle.so")
 
 SQEXP, MATERN32, MATERN12, MATERN52 = 0, 1, 2, 3
+OMEGA_SRHT, OMEGA_GAUSS, OMEGA_DHT, OMEGA_DCT = 0, 1, 2, 3   # NEXT-1: Hartley / cosine structured Omega
 
 
 def build(force: bool = False) -> str:
@@ -67,6 +68,11 @@ def lib():
             "ko_back_substitute": (None, [P, i32, P, i32, i32, P]),
             "ko_omega_apply_srht": (None, [P, P, i64, i64, i32, P, i32, P]),
             "ko_omega_apply_gauss": (None, [P, i64, i32, P, i32, P]),
+            "ko_selection_n": (i, [u64, i64, i64, i32, P]),
+            "ko_trig_entry": (dbl, [i, i64, i64, i64]),
+            "ko_omega_trig": (None, [i, P, P, i64, i32, P]),
+            "ko_sketch_dense_rows": (None, [P, i64, i, i, dbl, dbl, dbl, P, i32, P, i64, P, i]),
+            "ko_omega_apply_dense": (None, [P, i64, i32, P, i32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -107,6 +113,32 @@ def selection(seed: int, N: int, d: int) -> np.ndarray:
     if lib().ko_selection(seed, N, d, _p(S)) != 0:
         raise ValueError("d > N")
     return S
+
+
+def selection_n(seed: int, n: int, d: int) -> np.ndarray:
+    """S uniform without replacement from [0, n) (rejection of masked draws >= n), sorted (NEXT-1)."""
+    S = np.zeros(d, dtype=np.int32)
+    if lib().ko_selection_n(seed, next_pow2(n), n, d, _p(S)) != 0:
+        raise ValueError("d > n")
+    return S
+
+
+def trig_entry(kind: int, n: int, j: int, k: int) -> float:
+    """T[j][k] of the orthonormal discrete Hartley (kind 2) or cosine DCT-II (kind 3) transform."""
+    return float(lib().ko_trig_entry(int(kind), int(n), int(j), int(k)))
+
+
+def trig_matrix(kind: int, n: int) -> np.ndarray:
+    return np.array([[trig_entry(kind, n, j, k) for k in range(n)] for j in range(n)])
+
+
+def omega_trig(kind: int, s: np.ndarray, S: np.ndarray, n: int) -> np.ndarray:
+    """Explicit structured Omega = diag(s) T[:, S] (n x d), c = 1 (T orthonormal)."""
+    d = S.shape[0]
+    Om = np.zeros((n, d))
+    lib().ko_omega_trig(int(kind), _p(np.ascontiguousarray(s, np.int8)), _p(np.ascontiguousarray(S, np.int32)), n, d,
+                        _p(Om))
+    return Om
 
 
 def gauss_omega_fp16(seed: int, n: int, d: int) -> np.ndarray:
@@ -191,8 +223,16 @@ class Problem:
     @property
     def S(self):
         if self._S is None:
-            self._S = selection(self.seed, self.N, self.d)
+            self._S = (selection(self.seed, self.N, self.d) if self.omega != OMEGA_DHT and self.omega != OMEGA_DCT
+                       else selection_n(self.seed, self.n, self.d))
         return self._S
+
+    @property
+    def omd(self):
+        """Explicit fp64 Omega of the Hartley / cosine kinds (n x d)."""
+        if getattr(self, "_omd", None) is None:
+            self._omd = omega_trig(self.omega, self.s, self.S, self.n)
+        return self._omd
 
     @property
     def om16(self):
@@ -205,8 +245,10 @@ class Problem:
 
     def omega_dense(self) -> np.ndarray:
         """Explicit Omega (n x d), tier A."""
-        if self.omega == 0:
+        if self.omega == OMEGA_SRHT:
             return omega_srht(self.s, self.S, self.n)
+        if self.omega in (OMEGA_DHT, OMEGA_DCT):
+            return self.omd
         return fp16_to_f64(self.om16) / np.sqrt(self.d)
 
     def sketch_tierA(self) -> np.ndarray:
@@ -218,7 +260,10 @@ class Problem:
         rows = np.arange(self.n, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
         Y = np.zeros((rows.shape[0], self.d))
         L = lib()
-        if self.omega == 0:
+        if self.omega in (OMEGA_DHT, OMEGA_DCT):
+            L.ko_sketch_dense_rows(_p(self.pts), self.n, self.dim, self.kind, self.sigma2, self.ell, self.nugget,
+                                   _p(self.omd), self.d, _p(rows), rows.shape[0], _p(Y), _threads(nthreads))
+        elif self.omega == 0:
             L.ko_sketch_srht_rows(_p(self.pts), self.n, self.dim, self.kind, self.sigma2, self.ell, self.nugget,
                                   _p(self.s), _p(self.S), self.N, self.d, _p(rows), rows.shape[0], _p(Y),
                                   _threads(nthreads))
@@ -232,7 +277,9 @@ class Problem:
         Z = np.ascontiguousarray(Z, np.float64)
         m = Z.shape[1]
         X = np.zeros((self.n, m))
-        if self.omega == 0:
+        if self.omega in (OMEGA_DHT, OMEGA_DCT):
+            lib().ko_omega_apply_dense(_p(self.omd), self.n, self.d, _p(Z), m, _p(X))
+        elif self.omega == 0:
             lib().ko_omega_apply_srht(_p(self.s), _p(self.S), self.n, self.N, self.d, _p(Z), m, _p(X))
         else:
             om = np.ascontiguousarray(self.om16)

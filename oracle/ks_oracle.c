@@ -226,6 +226,47 @@ void ko_matmul(const double* A, const double* B, int64_t m, int64_t p, int64_t k
     }
 }
 
+/* NEXT-1 structured Omega = R T P (Def. 1) with T the discrete Hartley or the discrete
+ * cosine transform (PAPER.md:74 "discrete cosine matrix, discrete Hartley matrix", :91 "Hartley and
+ * discrete cosine transforms ... do not have these problems"), both taken orthonormal so that c = 1
+ * (L1) and for any n (no padding).  P: uniform without replacement from [0, n) -- the selection stream
+ * masked to [0, N), N = 2^ceil(log2 n), out-of-range draws rejected (for n = N identical to
+ * ko_selection), sorted ascending. */
+int ko_selection_n(uint64_t seed, int64_t N, int64_t n, int32_t d, int32_t* S) {
+  if (d > n || d < 0 || n > N) return -1;
+  uint8_t* used = (uint8_t*)calloc((size_t)n, 1);
+  int32_t got = 0;
+  for (uint64_t t = 0; got < d; ++t) {
+    uint32_t w[4];
+    draw(seed, ST_SELECT, t, w);
+    uint32_t cand = w[0] & (uint32_t)(N - 1);
+    if (cand < (uint64_t)n && !used[cand]) { used[cand] = 1; ++got; }
+  }
+  int32_t k = 0;
+  for (int64_t j = 0; j < n; ++j) if (used[j]) S[k++] = (int32_t)j;
+  free(used);
+  return 0;
+}
+
+/* T[j][k]: kind 2 = discrete Hartley, cas(2 pi j k / n) / sqrt(n), cas = cos + sin;
+ *          kind 3 = discrete cosine (DCT-II), sqrt(2/n) eps_k cos(pi (2j+1) k / (2n)), eps_0 = 1/sqrt(2).
+ * The angle's integer part is reduced exactly (j k mod n, (2j+1) k mod 4n) before the fp64 cos/sin. */
+double ko_trig_entry(int kind, int64_t n, int64_t j, int64_t k) {
+  const double pi = 3.14159265358979323846;
+  if (kind == 2) {
+    const double a = 2.0 * pi * (double)((j * k) % n) / (double)n;
+    return (cos(a) + sin(a)) / sqrt((double)n);
+  }
+  const double a = pi * (double)(((2 * j + 1) * k) % (4 * n)) / (2.0 * (double)n);
+  return sqrt(2.0 / (double)n) * (k == 0 ? 1.0 / sqrt(2.0) : 1.0) * cos(a);
+}
+
+/* Explicit Omega = diag(s) T[:, S] (n x d), row-major. */
+void ko_omega_trig(int kind, const int8_t* s, const int32_t* S, int64_t n, int32_t d, double* Om) {
+  for (int64_t j = 0; j < n; ++j)
+    for (int32_t t = 0; t < d; ++t) Om[j * d + t] = (double)s[j] * ko_trig_entry(kind, n, j, S[t]);
+}
+
 /* ------------------------------------------------------------------------- */
 /* Tier B sketch: per row, Y[i,:] = (1/sqrt N) (H_N (s o K[i,:]))[S]            */
 /* (PAPER.md:19 "structured random matrices ... n log d", :61, :95).           */
@@ -234,13 +275,27 @@ typedef struct {
   const float* pts; int64_t n; int dim; int kind; double sigma2, ell, nugget;
   const int8_t* s; const int32_t* S; int64_t N; int32_t d;
   const uint16_t* om;                 /* gaussian omega (n x d fp16) or NULL */
+  const double* omd;                  /* dense fp64 omega (n x d) or NULL (structured Hartley / cosine) */
   const int64_t* rows; int64_t nrows; double* Y;
   int tid, nthreads;
 } sketch_job;
 
 static void* sketch_worker(void* arg) {
   sketch_job* J = (sketch_job*)arg;
-  if (J->om == NULL) {
+  if (J->omd != NULL) {
+    double* krow = (double*)malloc(sizeof(double) * (size_t)J->n);
+    for (int64_t r = J->tid; r < J->nrows; r += J->nthreads) {
+      int64_t i = J->rows[r];
+      for (int64_t j = 0; j < J->n; ++j)
+        krow[j] = ko_K_entry(J->pts, J->n, J->dim, J->kind, J->sigma2, J->ell, J->nugget, i, j);
+      for (int32_t t = 0; t < J->d; ++t) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < J->n; ++j) acc += krow[j] * J->omd[j * J->d + t];
+        J->Y[r * J->d + t] = acc;
+      }
+    }
+    free(krow);
+  } else if (J->om == NULL) {
     double* v = (double*)malloc(sizeof(double) * (size_t)J->N);
     double c = 1.0 / sqrt((double)J->N);
     for (int64_t r = J->tid; r < J->nrows; r += J->nthreads) {
@@ -286,7 +341,7 @@ static void run_sketch(sketch_job* base, int nthreads) {
 void ko_sketch_srht_rows(const float* pts, int64_t n, int dim, int kind, double sigma2, double ell,
                          double nugget, const int8_t* s, const int32_t* S, int64_t N, int32_t d,
                          const int64_t* rows, int64_t nrows, double* Y, int nthreads) {
-  sketch_job J = {pts, n, dim, kind, sigma2, ell, nugget, s, S, N, d, NULL, rows, nrows, Y, 0, 1};
+  sketch_job J = {pts, n, dim, kind, sigma2, ell, nugget, s, S, N, d, NULL, NULL, rows, nrows, Y, 0, 1};
   run_sketch(&J, nthreads);
 }
 
@@ -295,7 +350,14 @@ void ko_sketch_srht_rows(const float* pts, int64_t n, int dim, int kind, double 
 void ko_sketch_gauss_rows(const float* pts, int64_t n, int dim, int kind, double sigma2, double ell,
                           double nugget, const uint16_t* om, int32_t d, const int64_t* rows,
                           int64_t nrows, double* Y, int nthreads) {
-  sketch_job J = {pts, n, dim, kind, sigma2, ell, nugget, NULL, NULL, 0, d, om, rows, nrows, Y, 0, 1};
+  sketch_job J = {pts, n, dim, kind, sigma2, ell, nugget, NULL, NULL, 0, d, om, NULL, rows, nrows, Y, 0, 1};
+  run_sketch(&J, nthreads);
+}
+
+/* Structured Hartley / cosine Omega (NEXT-1): Y[i,:] = K[i,:] Omega with the explicit fp64 Omega. */
+void ko_sketch_dense_rows(const float* pts, int64_t n, int dim, int kind, double sigma2, double ell, double nugget,
+                          const double* Om, int32_t d, const int64_t* rows, int64_t nrows, double* Y, int nthreads) {
+  sketch_job J = {pts, n, dim, kind, sigma2, ell, nugget, NULL, NULL, 0, d, NULL, Om, rows, nrows, Y, 0, 1};
   run_sketch(&J, nthreads);
 }
 
@@ -549,5 +611,15 @@ void ko_omega_apply_gauss(const uint16_t* om, int64_t n, int32_t d, const double
       double acc = 0.0;
       for (int32_t t = 0; t < d; ++t) acc += ko_fp16_to_double(om[j * d + t]) * Z[t * m + col];
       X[j * m + col] = c * acc;
+    }
+}
+
+/* X = Omega Z with an explicit fp64 Omega (n x d). */
+void ko_omega_apply_dense(const double* Om, int64_t n, int32_t d, const double* Z, int32_t m, double* X) {
+  for (int64_t j = 0; j < n; ++j)
+    for (int32_t col = 0; col < m; ++col) {
+      double acc = 0.0;
+      for (int32_t t = 0; t < d; ++t) acc += Om[j * d + t] * Z[t * m + col];
+      X[j * m + col] = acc;
     }
 }
