@@ -63,8 +63,14 @@ typedef enum ks_kernel_kind { KS_KERNEL_SQEXP = 0, KS_KERNEL_MATERN32 = 1 } ks_k
  *   KS_OMEGA_SRHT  Def. 1, T = Walsh-Hadamard (:74-89):
  *                  Omega = D_s H_N[:, S] / sqrt(N), natural order, N = 2^ceil(log2 n),
  *                  K zero-padded to N columns (readings L1-L4).
- *   KS_OMEGA_GAUSS PAPER.md:54: Omega_ij = fp16_RN(z_ij) / sqrt(d), z ~ N(0,1) (L6). */
-typedef enum ks_omega_kind { KS_OMEGA_SRHT = 0, KS_OMEGA_GAUSS = 1 } ks_omega_kind;
+ *   KS_OMEGA_GAUSS PAPER.md:54: Omega_ij = fp16_RN(z_ij) / sqrt(d), z ~ N(0,1) (L6).
+ *   KS_OMEGA_DHT / KS_OMEGA_DCT (NEXT-1): Def. 1 with T the orthonormal discrete Hartley
+ *                  (cas(2 pi j k / n) / sqrt n) or cosine (DCT-II) transform (the
+ *                  "HP" / "HC" projections of :403), for any n (no padding): Omega = D_s T[:, S],
+ *                  S uniform without replacement from [0, n) (masked Philox draws >= n rejected).
+ *                  Computed as a dense tensor-core contraction with Omega generated once per call in
+ *                  fp16 hi + lo (scaled by sqrt n); same d limits as GAUSS. */
+typedef enum ks_omega_kind { KS_OMEGA_SRHT = 0, KS_OMEGA_GAUSS = 1, KS_OMEGA_DHT = 2, KS_OMEGA_DCT = 3 } ks_omega_kind;
 
 typedef struct ks_sketch_desc {
   int64_t n;       /* number of points = order of K, n >= 1 */
@@ -73,7 +79,7 @@ typedef struct ks_sketch_desc {
   float sigma2;    /* > 0 */
   float ell;       /* > 0 */
   float nugget;    /* >= 0, added to K's diagonal by index (L9) */
-  int32_t d;       /* sketch width, 1 <= d <= N; SRHT: d <= 512; GAUSS: d % 16 == 0, 16 <= d <= 256 */
+  int32_t d;       /* sketch width, 1 <= d <= N; SRHT: d <= 512; GAUSS/DHT/DCT: d <= n, d % 16 == 0, 16 <= d <= 256 */
   uint64_t seed;   /* Philox4x32-10 key */
   int32_t omega;   /* ks_omega_kind */
   int32_t reserved;

@@ -18,7 +18,7 @@ import os
 import torch
 
 __all__ = [
-    "KsError", "SketchDesc", "SQEXP", "MATERN32", "SRHT", "GAUSS", "lib", "library_path",
+    "KsError", "SketchDesc", "SQEXP", "MATERN32", "SRHT", "GAUSS", "DHT", "DCT", "lib", "library_path",
     "ks_sketch_workspace_size", "ks_sketch", "ks_omega_export", "ks_omega_apply",
     "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr", "ks_qform", "TSQR_TREE", "TSQR_CHAIN",
     "ks_tsqr_workspace_size_ex", "ks_tsqr_create_ex", "ks_tsqr_apply_qt", "ks_tsqr_apply_q",
@@ -31,7 +31,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 library_path = os.path.join(_HERE, "libks_b200.so")
 
 SQEXP, MATERN32 = 0, 1
-SRHT, GAUSS = 0, 1
+SRHT, GAUSS, DHT, DCT = 0, 1, 2, 3   # ks_omega_kind (DHT / DCT: NEXT-1 structured Hartley / cosine)
 STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARGUMENT", 2: "KS_ERR_SINGULAR", 3: "KS_ERR_CUDA", 4: "KS_ERR_OOM",
           5: "KS_ERR_UNSUPPORTED", 6: "KS_ERR_NCCL"}
 

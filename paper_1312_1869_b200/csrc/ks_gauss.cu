@@ -144,7 +144,9 @@ KS_DEVINL void umma_commit_2cta(uint32_t bar) {
       : "memory");
 }
 
-template <int DIM, int KIND>
+// NB = 1: Gaussian Omega (one fp16 plane); NB = 2: Hartley / cosine Omega as fp16 hi + lo planes (NEXT-1),
+// a third MMA per K step (K_hi Omega_lo) and 3 pipeline stages (the B tiles double).
+template <int DIM, int KIND, int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGThreads, 1)
 k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmP,
                 const float4* __restrict__ pk, int64_t row_begin,
@@ -155,32 +157,34 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
   const int kh = blockIdx.y, nkb_a = gridDim.y > 1 ? nkb_all / 2 : nkb_all;
   const int kb0 = kh * nkb_a, nkb = kh ? nkb_all - nkb_a : nkb_a;
   float* __restrict__ Y = kh ? Y1 : Y0;
+  constexpr int NST = NB == 1 ? kG2Stages : 3;
   const int kBHalfBytes = (DN / 2) * kGaussBK * 2;
+  const int kBStage = NB * kBHalfBytes;
   const uint32_t kTmemCols = (2 * DN <= 32) ? 32 : (2 * DN <= 64) ? 64 : (2 * DN <= 128) ? 128 : (2 * DN <= 256) ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_hi = smem;
-  uint8_t* a_lo = smem + kG2Stages * kATileBytes;
-  uint8_t* b_t = a_lo + kG2Stages * kATileBytes;
+  uint8_t* a_lo = smem + NST * kATileBytes;
+  uint8_t* b_t = a_lo + NST * kATileBytes;
   // [kPtsStages][8 groups][8 points]: TMA SWIZZLE_128B stores point 8g + q of a stage at 16-B chunk q ^ g of
   // its 128-B row g, so the 8 lanes reading 8 different groups at the same q hit 8 different bank groups.
-  float4* pring = reinterpret_cast<float4*>(b_t + kG2Stages * kBHalfBytes);
+  float4* pring = reinterpret_cast<float4*>(b_t + NST * kBStage);
   uint64_t* bars = reinterpret_cast<uint64_t*>(pring + kPtsStages * kGaussBK);
   // full[S], empty[S], accf[2], acce[2], pfull[PS], pempty[PS], lfull[S]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kG2Stages + 4 + 2 * kPtsStages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 4 + 2 * kPtsStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int64_t row0 = row_begin + (int64_t)(blockIdx.x >> 1) * 256 + 128 * (int64_t)rank;
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kG2Stages);
-  const uint32_t accf0 = smem_u32(bars + 2 * kG2Stages), acce0 = smem_u32(bars + 2 * kG2Stages + 2);
-  const uint32_t pfull0 = smem_u32(bars + 2 * kG2Stages + 4), pempty0 = pfull0 + 8 * kPtsStages;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
+  const uint32_t accf0 = smem_u32(bars + 2 * NST), acce0 = smem_u32(bars + 2 * NST + 2);
+  const uint32_t pfull0 = smem_u32(bars + 2 * NST + 4), pempty0 = pfull0 + 8 * kPtsStages;
   const uint32_t lfull0 = pempty0 + 8 * kPtsStages;
   const uint32_t full0_L = mapa_u32(full0, 0), acce0_L = mapa_u32(acce0, 0);   // the leader's barriers
   const int nseg = (nkb + seg_kb - 1) / seg_kb;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kG2Stages; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(full0 + 8 * s, 8 + 1 + 1);   // leader's 8 producer warps + the peer's relay + expect_tx
       mbar_init(lfull0 + 8 * s, 8);           // peer: its 8 producer warps (relayed to the leader)
       mbar_init(empty0 + 8 * s, 1);
@@ -210,12 +214,15 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA: this CTA's half of the Omega^T tile (DN/2 x 64)
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kG2Stages;
-        const uint32_t ph = (kb / kG2Stages) & 1;
+        const int s = kb % NST;
+        const uint32_t ph = (kb / NST) & 1;
         mbar_wait(empty0 + 8 * s, ph ^ 1);
-        if (rank == 0) mbar_arrive_tx(full0 + 8 * s, 2 * kBHalfBytes);
-        tma_load_2d_2cta(smem_u32(b_t + s * kBHalfBytes), &tmB, (kb0 + kb) * kGaussBK, (int)rank * (DN / 2),
+        if (rank == 0) mbar_arrive_tx(full0 + 8 * s, 2 * kBStage);
+        tma_load_2d_2cta(smem_u32(b_t + s * kBStage), &tmB, (kb0 + kb) * kGaussBK, (int)rank * (DN / 2),
                          full0_L + 8 * s);
+        if (NB == 2)   // the lo plane: rows DN .. 2 DN of the stacked Omega^T
+          tma_load_2d_2cta(smem_u32(b_t + s * kBStage + kBHalfBytes), &tmB, (kb0 + kb) * kGaussBK,
+                           DN + (int)rank * (DN / 2), full0_L + 8 * s);
       }
     }
   } else if (warp == 3) {
@@ -224,8 +231,8 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
     // collects the 8 producer warps on a local barrier and issues one cluster-scope arrive per stage.
     if (rank == 1 && lane == 0) {
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kG2Stages;
-        mbar_wait(lfull0 + 8 * s, (kb / kG2Stages) & 1);
+        const int s = kb % NST;
+        mbar_wait(lfull0 + 8 * s, (kb / NST) & 1);
         asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(full0_L + 8 * s) : "memory");
       }
     }
@@ -248,18 +255,20 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
         const uint32_t dtm = tmem;
         const int kb1 = min(nkb, (g + 1) * seg_kb);
         for (int kb = g * seg_kb; kb < kb1; ++kb) {
-          const int s = kb % kG2Stages;
-          const uint32_t ph = (kb / kG2Stages) & 1;
+          const int s = kb % NST;
+          const uint32_t ph = (kb / NST) & 1;
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
           const uint64_t dh = umma_desc_sw128(smem_u32(a_hi + s * kATileBytes));
           const uint64_t dl = umma_desc_sw128(smem_u32(a_lo + s * kATileBytes));
-          const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBHalfBytes));
+          const uint64_t db = umma_desc_sw128(smem_u32(b_t + s * kBStage));
+          const uint64_t dbl = umma_desc_sw128(smem_u32(b_t + s * kBStage + kBHalfBytes));
 #pragma unroll
           for (int kk = 0; kk < kGaussBK / 16; ++kk) {
             if (!(dbg & 1)) {   // timing studies only (KS_GAUSS_DEBUG): bit 0 skips the MMAs
               umma_f16_2cta(dtm, dh + 2 * kk, db + 2 * kk, idesc, (kb != g * seg_kb || kk != 0) ? 1u : 0u);
               umma_f16_2cta(dtm, dl + 2 * kk, db + 2 * kk, idesc, 1u);
+              if (NB == 2) umma_f16_2cta(dtm, dh + 2 * kk, dbl + 2 * kk, idesc, 1u);
             }
           }
           umma_commit_2cta(empty0 + 8 * s);
@@ -286,8 +295,8 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       xi2[pr][0] = f2(q[0].x, q[1].x); xi2[pr][1] = f2(q[0].y, q[1].y); xi2[pr][2] = f2(q[0].z, q[1].z);
     }
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kG2Stages;
-      const uint32_t ph = (kb / kG2Stages) & 1;
+      const int s = kb % NST;
+      const uint32_t ph = (kb / NST) & 1;
       const int64_t j0 = (int64_t)(kb0 + kb) * kGaussBK + 8 * cq;
       const int ps = kb % kPtsStages;
       mbar_wait(pfull0 + 8 * ps, (kb / kPtsStages) & 1);
@@ -390,13 +399,13 @@ static int gauss_seg_kb() {
   return v;
 }
 
-template <int DIM, int KIND>
+template <int DIM, int KIND, int NB>
 static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
                               char* ws, cudaStream_t st) {
   auto encode = get_encode();
   if (!encode) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int DN = D.d;
-  cuuint64_t dims[2] = {(cuuint64_t)L.ncols_pad, (cuuint64_t)DN};
+  cuuint64_t dims[2] = {(cuuint64_t)L.ncols_pad, (cuuint64_t)(NB * DN)};   // NB = 2: hi plane over lo plane
   cuuint64_t strides[1] = {(cuuint64_t)L.ncols_pad * 2};
   cuuint32_t estr[2] = {1, 1};
   CUtensorMap tm2;   // half-width boxes (DN/2 rows of Omega^T) for the CTA pair
@@ -415,9 +424,12 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   if (r != CUDA_SUCCESS) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled (points) failed: " + std::to_string((int)r));
   const int nkb = (int)(L.ncols_pad / kGaussBK);
   const double S = gauss_scale(D);
-  const float nug = (float)(S * D.nugget), osc = (float)(1.0 / (S * std::sqrt((double)D.d)));
+  // Gaussian: Omega = fp16 / sqrt(d); Hartley / cosine: the planes hold Omega * sqrt(n)
+  const float nug = (float)(S * D.nugget),
+              osc = (float)(1.0 / (S * std::sqrt((double)(NB == 1 ? D.d : D.n))));
   const float4* pk = reinterpret_cast<const float4*>(ws + L.off_pk);
-  const int smem = 1024 + kG2Stages * (2 * kATileBytes + (DN / 2) * kGaussBK * 2) + kPtsStages * kPtsBytes + 512;
+  constexpr int NST = NB == 1 ? kG2Stages : 3;
+  const int smem = 1024 + NST * (2 * kATileBytes + NB * (DN / 2) * kGaussBK * 2) + kPtsStages * kPtsBytes + 512;
   // split the column blocks in two when the row tiles leave a partial last wave (one CTA pair per 2 SMs)
   static const int pair_slots = [] {
     int dev = 0, sms = 148;
@@ -428,11 +440,13 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   const int64_t pairs = (re - rb + 255) / 256;
   const int ksplit = (nkb >= 2 && pairs % pair_slots != 0 && pairs < 16 * pair_slots) ? 2 : 1;
   float* Y1 = reinterpret_cast<float*>(ws + L.off_ybuf);
-  auto kern = k_sketch_gauss2<DIM, KIND>;
+  auto kern = k_sketch_gauss2<DIM, KIND, NB>;
   KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const dim3 grid(2u * (unsigned)pairs, (unsigned)ksplit);
   static const int dbg = [] { const char* e = getenv("KS_GAUSS_DEBUG"); return e ? atoi(e) : 0; }();
-  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, gauss_seg_kb(), DN, nug, osc, Y, Y1, dbg);
+  // NB = 2 issues 3 MMAs per K step: 11 stages per segment keep the non-RN accumulation run as for NB = 1
+  const int seg = NB == 1 ? gauss_seg_kb() : std::max(1, gauss_seg_kb() * 2 / 3);
+  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, seg, DN, nug, osc, Y, Y1, dbg);
   KS_LAUNCH_CHECK();
   if (ksplit == 2) {
     const int64_t tot = (re - rb) * (int64_t)DN;
@@ -443,16 +457,23 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   return KS_OK;
 }
 
+template <int DIM, int KIND>
+static ks_status launch_gauss_nb(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
+                                 char* ws, cudaStream_t st) {
+  return D.omega == KS_OMEGA_GAUSS ? launch_gauss<DIM, KIND, 1>(D, L, rb, re, Y, ws, st)
+                                   : launch_gauss<DIM, KIND, 2>(D, L, rb, re, Y, ws, st);
+}
+
 ks_status gauss_sketch_run(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
                            char* ws, cudaStream_t st) {
   const bool se = D.kernel == KS_KERNEL_SQEXP;
   switch (D.dim) {
-    case 1: return se ? launch_gauss<1, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
-                      : launch_gauss<1, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
-    case 2: return se ? launch_gauss<2, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
-                      : launch_gauss<2, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
-    case 3: return se ? launch_gauss<3, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
-                      : launch_gauss<3, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
+    case 1: return se ? launch_gauss_nb<1, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
+                      : launch_gauss_nb<1, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
+    case 2: return se ? launch_gauss_nb<2, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
+                      : launch_gauss_nb<2, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
+    case 3: return se ? launch_gauss_nb<3, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)
+                      : launch_gauss_nb<3, KS_KERNEL_MATERN32>(D, L, rb, re, Y, ws, st);
   }
   return fail(KS_ERR_INVALID_ARGUMENT, "dim");
 }

@@ -35,7 +35,7 @@ SketchLayout sketch_layout(const ks_sketch_desc& desc) {
     while (64 * tpo < desc.d) tpo *= 2;   // 64 output groups in the gather phase
     L.tpo = tpo;
     L.d_pad = 64 * tpo;
-  } else {
+  } else {   // GAUSS, DHT, DCT: the tensor-core contraction
     L.A = 0;
     L.ncols_pad = (desc.n + kGaussBK - 1) / kGaussBK * kGaussBK;
     if (L.ncols_pad < kGaussBM) L.ncols_pad = kGaussBM;
@@ -51,11 +51,12 @@ SketchLayout sketch_layout(const ks_sketch_desc& desc) {
   L.off_bucket_ofs = take(sizeof(int32_t) * (kSrhtB + 1));
   L.off_bucket_idx = take(sizeof(int32_t) * 512);
   L.off_bitmap = take(sizeof(uint32_t) * (size_t)((L.N + 31) / 32));
-  L.off_gauss = take(desc.omega == KS_OMEGA_GAUSS ? sizeof(__half) * (size_t)desc.d * (size_t)L.ncols_pad : 0);
+  const int om_planes = desc.omega == KS_OMEGA_GAUSS ? 1 : (desc.omega == KS_OMEGA_SRHT ? 0 : 2);   // trig: hi + lo
+  L.off_gauss = take(sizeof(__half) * (size_t)om_planes * (size_t)desc.d * (size_t)L.ncols_pad);
   L.off_perm = take(desc.omega == KS_OMEGA_SRHT ? sizeof(int32_t) * (size_t)L.d_pad : 0);
   L.off_sgn = take(desc.omega == KS_OMEGA_SRHT ? sizeof(float) * (size_t)L.A * (size_t)L.d_pad : 0);
   // Gaussian split-K: the second half's partial Y (rows x d)
-  L.off_ybuf = take(desc.omega == KS_OMEGA_GAUSS ? sizeof(float) * (size_t)desc.n * (size_t)desc.d : 0);
+  L.off_ybuf = take(desc.omega != KS_OMEGA_SRHT ? sizeof(float) * (size_t)desc.n * (size_t)desc.d : 0);
   L.bytes = off;
   return L;
 }
@@ -75,8 +76,8 @@ ks_status sketch_validate(const ks_sketch_desc* desc) {
   if (D.d < 1 || D.d > N) return fail(KS_ERR_INVALID_ARGUMENT, "need 1 <= d <= N");
   if (D.omega == KS_OMEGA_SRHT) {
     if (D.d > 512) return fail(KS_ERR_UNSUPPORTED, "SRHT path supports d <= 512");
-  } else if (D.omega == KS_OMEGA_GAUSS) {
-    if (D.d > D.n) return fail(KS_ERR_INVALID_ARGUMENT, "Gaussian sketch needs d <= n");
+  } else if (D.omega == KS_OMEGA_GAUSS || D.omega == KS_OMEGA_DHT || D.omega == KS_OMEGA_DCT) {
+    if (D.d > D.n) return fail(KS_ERR_INVALID_ARGUMENT, "Gaussian / Hartley / cosine sketch needs d <= n");
     if (D.d % 16 != 0 || D.d < 16 || D.d > 256)
       return fail(KS_ERR_UNSUPPORTED, "Gaussian tcgen05 path needs d % 16 == 0 and 16 <= d <= 256");
   } else {
@@ -132,7 +133,7 @@ KS_DEVINL int block_rank(bool flag, int* wsum, int* total) {
 //             sits in the 8-bank group cls(m) = (m + (m >> 5)) & 3 equal to og & 3, so the four groups of a
 //             quarter-warp read distinct banks; outputs left over fill the remaining slots in order.
 constexpr int64_t kSelSmemBits = int64_t(1) << 20;
-__global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, int d, int d_pad, int tpo,
+__global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, int64_t range, int d, int d_pad, int tpo,
                                                     uint32_t* __restrict__ gbitmap, int32_t* __restrict__ sel,
                                                     uint32_t* __restrict__ tab, int32_t* __restrict__ bofs,
                                                     int32_t* __restrict__ bidx, int32_t* __restrict__ perm) {
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, in
       const uint32_t c = philox(seed, kStreamSelect, base + (uint64_t)lane).x & (uint32_t)(N - 1);
       const unsigned same = __match_any_sync(0xffffffffu, c);
       const uint32_t word = in_smem ? bitmap[c >> 5] : __ldcg(bitmap + (c >> 5));
-      const bool keep = (__ffs(same) - 1) == lane && !((word >> (c & 31)) & 1u);
+      const bool keep = (__ffs(same) - 1) == lane && !((word >> (c & 31)) & 1u) && (int64_t)c < range;
       const unsigned ball = __ballot_sync(0xffffffffu, keep);
       const int pos = count + __popc(ball & ((1u << lane) - 1u));
       if (keep && pos < d) atomicOr(bitmap + (c >> 5), 1u << (c & 31));
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, in
   }
   __syncthreads();
   if (act) bidx[tid] = s_left[tid];
+  if (tpo == 0) return;   // Hartley / cosine: no SRHT gather permutation
   // ---- perm
   const int h = (m + (m >> 5)) & 3;
   int rank[4], ncls[4];
@@ -280,6 +282,35 @@ __global__ void k_gauss_omega(uint64_t seed, int64_t n, int d, int64_t ncols_pad
   omT[(int64_t)t * ncols_pad + j] = h;
 }
 
+// NEXT-1: structured Omega^T (d x ncols_pad) = (D_s T[:, S])^T * sqrt(n) in fp16 hi + lo, T the orthonormal
+// discrete Hartley (kind DHT: cas(2 pi j k / n) / sqrt n) or cosine DCT-II (sqrt(2/n) eps_k cos(pi (2j+1) k / 2n))
+// transform; the sqrt(n) scale keeps the entries O(1) so that lo = fp16(v - hi) stays a normal number for
+// typical entries (|v - hi - lo| <~ 2^-22 |v|).  The angle's integer part is reduced exactly, then fp64
+// sincospi.  Columns j >= n are zero.
+__global__ void k_trig_omega(uint64_t seed, int64_t n, int d, int64_t ncols_pad, int kind,
+                             const int32_t* __restrict__ sel, __half* __restrict__ hi, __half* __restrict__ lo) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  if (j >= ncols_pad) return;
+  __half h = __float2half_rn(0.f), l = __float2half_rn(0.f);
+  if (j < n) {
+    const int64_t k = sel[t];
+    double v;
+    if (kind == KS_OMEGA_DHT) {
+      double sn, cs;
+      sincospi(2.0 * (double)((j * k) % n) / (double)n, &sn, &cs);
+      v = cs + sn;
+    } else {
+      v = (k == 0 ? 1.0 : 1.4142135623730951) * cospi((double)(((2 * j + 1) * k) % (4 * n)) / (2.0 * (double)n));
+    }
+    v *= (double)rademacher(seed, j);
+    h = __double2half(v);
+    l = __double2half(v - (double)__half2float(h));
+  }
+  hi[(int64_t)t * ncols_pad + j] = h;
+  lo[(int64_t)t * ncols_pad + j] = l;
+}
+
 double gauss_scale(const ks_sketch_desc& D) {
   const double kmax = (double)D.sigma2 + (double)D.nugget;
   int e = (int)std::floor(std::log2(16384.0 / kmax));
@@ -302,14 +333,14 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
                                                  srht, reinterpret_cast<float4*>(ws + L.off_pk));
     KS_LAUNCH_CHECK();
   }
+  static bool attr = false;
+  if (!attr) {
+    KS_CUDA_TRY(cudaFuncSetAttribute(k_selection, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelSmemBits / 8)));
+    attr = true;
+  }
+  const int sel_smem = L.N <= kSelSmemBits ? (int)((L.N + 31) / 32 * 4) : 0;
   if (srht) {
-    static bool attr = false;
-    if (!attr) {
-      KS_CUDA_TRY(cudaFuncSetAttribute(k_selection, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelSmemBits / 8)));
-      attr = true;
-    }
-    const int sel_smem = L.N <= kSelSmemBits ? (int)((L.N + 31) / 32 * 4) : 0;
-    k_selection<<<1, 1024, sel_smem, st>>>(D.seed, L.N, D.d, L.d_pad, L.tpo,
+    k_selection<<<1, 1024, sel_smem, st>>>(D.seed, L.N, L.N, D.d, L.d_pad, L.tpo,
                                            reinterpret_cast<uint32_t*>(ws + L.off_bitmap),
                                            reinterpret_cast<int32_t*>(ws + L.off_sel),
                                            reinterpret_cast<uint32_t*>(ws + L.off_tab),
@@ -322,9 +353,22 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
                                                                reinterpret_cast<const int32_t*>(ws + L.off_perm),
                                                                L.d_pad, L.A, reinterpret_cast<float*>(ws + L.off_sgn));
     KS_LAUNCH_CHECK();
-  } else {
+  } else if (D.omega == KS_OMEGA_GAUSS) {
     dim3 grid((unsigned)((L.ncols_pad + 255) / 256), (unsigned)D.d);
     k_gauss_omega<<<grid, 256, 0, st>>>(D.seed, D.n, D.d, L.ncols_pad, reinterpret_cast<__half*>(ws + L.off_gauss));
+    KS_LAUNCH_CHECK();
+  } else {   // Hartley / cosine: S from [0, n) by rejection, then Omega^T (hi, lo)
+    k_selection<<<1, 1024, sel_smem, st>>>(D.seed, L.N, D.n, D.d, 0, 0, reinterpret_cast<uint32_t*>(ws + L.off_bitmap),
+                                           reinterpret_cast<int32_t*>(ws + L.off_sel),
+                                           reinterpret_cast<uint32_t*>(ws + L.off_tab),
+                                           reinterpret_cast<int32_t*>(ws + L.off_bucket_ofs),
+                                           reinterpret_cast<int32_t*>(ws + L.off_bucket_idx), nullptr);
+    KS_LAUNCH_CHECK();
+    __half* hi = reinterpret_cast<__half*>(ws + L.off_gauss);
+    dim3 grid((unsigned)((L.ncols_pad + 255) / 256), (unsigned)D.d);
+    k_trig_omega<<<grid, 256, 0, st>>>(D.seed, D.n, D.d, L.ncols_pad, D.omega,
+                                       reinterpret_cast<const int32_t*>(ws + L.off_sel), hi,
+                                       hi + (size_t)D.d * L.ncols_pad);
     KS_LAUNCH_CHECK();
   }
   return KS_OK;
@@ -515,7 +559,7 @@ static ks_status dispatch_tpo(const SketchLayout& L, const ks_sketch_desc& D, in
 ks_status sketch_run(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y, char* ws,
                      cudaStream_t st) {
   if (re <= rb) return KS_OK;
-  if (D.omega == KS_OMEGA_GAUSS) return gauss_sketch_run(D, L, rb, re, Y, ws, st);
+  if (D.omega != KS_OMEGA_SRHT) return gauss_sketch_run(D, L, rb, re, Y, ws, st);   // Gaussian, Hartley, cosine
   const bool se = D.kernel == KS_KERNEL_SQEXP;
   switch (D.dim) {
     case 1: return se ? dispatch_tpo<1, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)
@@ -573,8 +617,8 @@ __global__ void __launch_bounds__(256) k_omega_apply_srht(const float* __restric
 }
 
 // Gaussian: X[j, :] = (1/sqrt d) sum_t Omega[j, t] Z[t, :].
-__global__ void __launch_bounds__(256) k_omega_apply_gauss(const __half* __restrict__ omT, int64_t ldo,
-                                                           const float* __restrict__ Z, int m, int d,
+__global__ void __launch_bounds__(256) k_omega_apply_gauss(const __half* __restrict__ omT, const __half* __restrict__ omT_lo,
+                                                           int64_t ldo, const float* __restrict__ Z, int m, int d,
                                                            int64_t row_begin, int64_t row_end, float scale,
                                                            float* __restrict__ X) {
   extern __shared__ float zs[];  // d x m
@@ -586,7 +630,8 @@ __global__ void __launch_bounds__(256) k_omega_apply_gauss(const __half* __restr
   for (int c0 = 0; c0 < m; c0 += 8) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int t = 0; t < d; ++t) {
-      const float o = __half2float(omT[(int64_t)t * ldo + j]);
+      float o = __half2float(omT[(int64_t)t * ldo + j]);
+      if (omT_lo) o += __half2float(omT_lo[(int64_t)t * ldo + j]);
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (c0 + q < m) acc[q] = fmaf(o, zs[t * m + c0 + q], acc[q]);
@@ -613,8 +658,11 @@ ks_status omega_apply_run(const ks_sketch_desc& D, const SketchLayout& L, const 
     const int smem = D.d * m * (int)sizeof(float);
     KS_CUDA_TRY(cudaFuncSetAttribute(k_omega_apply_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const unsigned grid = (unsigned)((re - rb + 255) / 256);
-    k_omega_apply_gauss<<<grid, 256, smem, st>>>(reinterpret_cast<const __half*>(ws + L.off_gauss), L.ncols_pad, Z,
-                                                  m, D.d, rb, re, (float)(1.0 / std::sqrt((double)D.d)), X);
+    const __half* hi = reinterpret_cast<const __half*>(ws + L.off_gauss);
+    const bool trig = D.omega != KS_OMEGA_GAUSS;   // Hartley / cosine: hi + lo, scaled by sqrt(n)
+    k_omega_apply_gauss<<<grid, 256, smem, st>>>(hi, trig ? hi + (size_t)D.d * L.ncols_pad : nullptr, L.ncols_pad, Z,
+                                                  m, D.d, rb, re,
+                                                  (float)(1.0 / std::sqrt((double)(trig ? D.n : D.d))), X);
     KS_LAUNCH_CHECK();
   }
   return KS_OK;
@@ -640,7 +688,7 @@ ks_status omega_export_run(const ks_sketch_desc& D, const SketchLayout& L, int8_
     KS_LAUNCH_CHECK();
   }
   if (sel) {
-    if (D.omega != KS_OMEGA_SRHT) return fail(KS_ERR_INVALID_ARGUMENT, "selection exists only for SRHT");
+    if (D.omega == KS_OMEGA_GAUSS) return fail(KS_ERR_INVALID_ARGUMENT, "no selection for the Gaussian Omega");
     KS_CUDA_TRY(cudaMemcpyAsync(sel, ws + L.off_sel, sizeof(int32_t) * (size_t)D.d, cudaMemcpyDeviceToDevice, st));
   }
   if (gauss) {

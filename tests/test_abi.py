@@ -40,7 +40,7 @@ def test_sketch_descriptor_layout_matches_header():
 
 
 @pytest.mark.parametrize("field,value", [("n", 0), ("dim", 4), ("ell", 0.0), ("sigma2", -1.0), ("nugget", -1e-3),
-                                         ("d", 0), ("kernel", 7), ("omega", 3)])
+                                         ("d", 0), ("kernel", 7), ("omega", 4)])
 def test_workspace_query_rejects_invalid_descriptors(field, value):
     import paper_1312_1869_b200 as ks
     args = dict(n=1024, dim=2, kernel=0, sigma2=1.0, ell=0.1, nugget=0.0, d=64, seed=1, omega=0)

@@ -319,3 +319,42 @@ def test_invalid_arguments_rejected_before_launch(ks, cuda):
     with pytest.raises(ks.KsError) as e:
         ks.ks_sketch(desc_of(cfg), _t(pts, cuda), 0, 10, torch.empty((10, 64), device=cuda), sk.ws[:100])
     assert e.value.status == 4
+
+
+# ---------------------------------------------------------------- NEXT-1: Hartley / cosine structured Omega
+TRIG_CASES = [
+    (2, dict(n=4096, d=128, dim=2)),                           # Hartley, SE, power-of-two n
+    (3, dict(n=3000, d=64, dim=1, kernel=1, ell=0.05)),        # cosine, Matern, ragged n (no padding)
+    (2, dict(n=1000, d=16, dim=3)),                            # Hartley, D = 3, smallest width
+    (3, dict(n=8192, d=256, dim=2)),                           # cosine, d = 256
+    (2, dict(n=5000, d=96, dim=2, kernel=1)),                  # Hartley, Matern, ragged tiles
+]
+
+
+@pytest.mark.parametrize("omega,over", TRIG_CASES)
+def test_trig_randomness_and_sketch_match_oracle(ks, cuda, omega, over):
+    """Signs and the selection from [0, n) bit-exact; Y = K R T P within 1e-5 of the fp64 oracle."""
+    cfg, pts, A, prob = problem("c2", omega=omega, seed=4321 + over["n"], **over)
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    Yg = sk(_t(pts, cuda)).cpu().numpy()
+    s, S, _ = sk.export(signs=True, sel=True, gauss=False)
+    assert np.array_equal(s.cpu().numpy(), prob.s)
+    assert np.array_equal(S.cpu().numpy(), prob.S)
+    assert relF(Yg, prob.sketch_rows()) <= Y_TOL
+
+
+@pytest.mark.parametrize("omega", [2, 3])
+def test_trig_omega_apply_matches_oracle(ks, cuda, omega):
+    cfg, pts, A, prob = problem("c2", n=3000, d=64, omega=omega, dim=2)
+    Z = np.random.default_rng(2).standard_normal((64, 5)).astype(np.float32)
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    X = sk.omega_apply(_t(Z, cuda)).cpu().numpy()
+    assert relF(X, prob.omega_apply(Z.astype(np.float64))) <= 1e-5
+
+
+@pytest.mark.parametrize("omega", [2, 3])
+def test_trig_lowrank_solve_matches_oracle(ks, cuda, omega):
+    cfg, pts, A, prob = problem("c1", omega=omega, d=64)
+    _solve_parity(ks, cuda, cfg, pts, A, prob)
+    cfg, pts, A, prob = problem("c2", omega=omega, n=6000, d=128, blocks=4)
+    _solve_parity(ks, cuda, cfg, pts, A, prob)
