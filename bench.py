@@ -127,7 +127,7 @@ def blocks_for(cfg, world):
 def make_config(name, cfg, world):
     return {"workload": name, "n": cfg["n"], "d": cfg["d"], "dim": cfg["dim"],
             "kernel": "sqexp" if cfg["kernel"] == 0 else "matern32",
-            "omega": "srht" if cfg["omega"] == 0 else "gauss", "blocks_per_gpu": blocks_for(cfg, world),
+            "omega": ["srht", "gauss", "hartley", "cosine"][cfg["omega"]], "blocks_per_gpu": blocks_for(cfg, world),
             "m": cfg["m"], "parallelism": f"rows x{world}",
             "l2": "flushed (256 MiB write) before every timed step"}
 
@@ -345,11 +345,12 @@ def run_ours(args, cfg, pts_np, A_np):
                     "kernel": "k_sketch_srht", "ops_per_element": ops_elem,
                     "peak_basis": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
         else:
-            flops = 2.0 * units * d * 2  # hi/lo split: 2 MMAs per element (split counted)
+            nmma = 2 if cfg["omega"] == ks_inputs.OMEGA_GAUSS else 3   # MMAs per K step (hi/lo splits counted)
+            flops = 2.0 * units * d * nmma
             achieved = flops / (t_sk * 1e-3) / 1e12
             peak = float(peaks.get("bf16_tflops", 1590.0))
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None, "kernel": "k_sketch_gauss2",
+                    "frac": achieved / peak, "traffic": None, "kernel": "k_sketch_gauss2", "mma_per_kstep": nmma,
                     "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst); fp16 dense = bf16 rate"}
         try:   # DRAM bytes of one launch of this config's sketch kernel from a committed ncu capture
             tr = json.load(open(TRAFFIC_PATH)).get(args.config) if world == 1 else None

@@ -126,7 +126,11 @@ CONFIGS = {
     "c5": dict(n=1048576, dim=2, dist="normal", kernel=MATERN32, sigma2=1.0, ell=0.3, nugget=1e-4,
                d=256, omega=OMEGA_SRHT, blocks=1, m=8, blocks_per_gpu=True),
 }
-CONFIG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
+# NEXT-1 measurement variants (not BASELINE configs): c3's problem with the paper's Hartley ("HP") and
+# cosine ("HC") structured projections (Table 3).
+CONFIGS["c3h"] = dict(CONFIGS["c3"], omega=OMEGA_DHT)
+CONFIGS["c3c"] = dict(CONFIGS["c3"], omega=OMEGA_DCT)
+CONFIG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5, "c3h": 3, "c3c": 3}
 
 
 def config_seed(name: str) -> int:
