@@ -129,9 +129,7 @@ KS_DEVINL int block_rank(bool flag, int* wsum, int* total) {
 // threads enumerate the bitmap in order.  Also builds, for the sketch and the Omega-apply:
 //   tab[t]  = m_t | a_t << 16 (kSrhtB-chunks),
 //   bofs/bidx = CSR of t by bucket m_t, ascending t inside a bucket,
-//   perm[s] = the gather slot permutation of the sketch: slot s = og*tpo + k prefers outputs whose F row
-//             sits in the 8-bank group cls(m) = (m + (m >> 5)) & 3 equal to og & 3, so the four groups of a
-//             quarter-warp read distinct banks; outputs left over fill the remaining slots in order.
+//   perm[s] = the gather slot permutation of the sketch (bank-conflict-free bins, see the perm section).
 constexpr int64_t kSelSmemBits = int64_t(1) << 20;
 __global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, int64_t range, int d, int d_pad, int tpo,
                                                     uint32_t* __restrict__ gbitmap, int32_t* __restrict__ sel,
@@ -141,6 +139,8 @@ __global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, in
   __shared__ int s_sel[512];
   __shared__ int s_lst[4][512];         // outputs of each class, ascending t
   __shared__ int s_left[512];
+  __shared__ int s_over[512];
+  __shared__ int s_moved[512];
   __shared__ int s_hist[kSrhtB + 1];
   __shared__ int s_fill[kSrhtB];
   __shared__ int wsum[32];
@@ -233,29 +233,83 @@ __global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, in
   __syncthreads();
   if (act) bidx[tid] = s_left[tid];
   if (tpo == 0) return;   // Hartley / cosine: no SRHT gather permutation
-  // ---- perm
+  // ---- perm.  Slot s = og*tpo + k is read by quarter-warp lanes of column og & 3 at bin (og >> 2)*tpo + k;
+  // a bin's four columns are conflict-free when their outputs sit in distinct 8-bank classes
+  // cls(m) = (m + (m >> 5)) & 3, or share one m (a broadcast).  Column c takes class c's outputs; a class
+  // with more than G = d_pad/4 outputs moves e_c = n_c - G of them as pairs of equal m: one bin holds
+  // both halves of a pair (its own column and a spare column of an under-full class), which frees one
+  // slot of column c.  Outputs left over (too few pairs) fill the remaining empty slots in order.
+  const int G = d_pad / 4;
   const int h = (m + (m >> 5)) & 3;
-  int rank[4], ncls[4];
+  int ncls[4];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) rank[c] = block_rank(act && h == c, wsum, &ncls[c]);
-  int myrank = 0;
+  for (int c = 0; c < 4; ++c) (void)block_rank(act && h == c, wsum, &ncls[c]);
+  int e[4], sp[4], Eb[5], Sb[5];
+  Eb[0] = Sb[0] = 0;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) myrank = (c == h) ? rank[c] : myrank;
-  if (act) s_lst[h][myrank] = tid;
-  const int per_cls = d_pad / 4;   // slots of each class
-  int nleft = 0;
-  const int lrank = block_rank(act && myrank >= per_cls, wsum, &nleft);   // (its barriers publish s_lst)
-  if (act && myrank >= per_cls) s_left[lrank] = tid;
-  // slot s: class og & 3, index inside its class (og >> 2) * tpo + k
+  for (int c = 0; c < 4; ++c) {
+    e[c] = max(0, ncls[c] - G);
+    sp[c] = max(0, G - ncls[c]);
+    Eb[c + 1] = Eb[c] + e[c];
+    Sb[c + 1] = Sb[c] + sp[c];
+  }
+  const int E = min(Eb[4], G);
+  for (int i = tid; i < 4 * 512; i += 1024) (&s_lst[0][0])[i] = -1;
+  if (tid < 512) s_moved[tid] = 0;
+  // pair leaders, in bucket order (equal m adjacent): positions 0, 2, 4, ... of a bucket with a successor
+  bool lead = false;
+  int lt = 0, lp = 0, lc = 0;
+  if (tid < d) {
+    lt = s_left[tid];
+    const int lm = s_sel[lt] & (kSrhtB - 1);
+    lead = ((tid - s_hist[lm]) & 1) == 0 && tid + 1 < s_hist[lm + 1];
+    lp = lead ? s_left[tid + 1] : 0;
+    lc = (lm + (lm >> 5)) & 3;
+  }
+  int pr = 0, le = 0, lEb = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {   // (the first barrier publishes the initialisation above)
+    int tot;
+    const int r = block_rank(lead && lc == c, wsum, &tot);
+    if (lc == c) { pr = r; le = e[c]; lEb = Eb[c]; }
+  }
+  if (lead && pr < le && lEb + pr < G) {
+    const int mv = lEb + pr;
+    int u = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) u = (Sb[c] <= mv && mv < Sb[c + 1]) ? c : u;
+    s_lst[lc][mv] = lt;
+    s_lst[u][mv] = lp;
+    s_moved[lt] = 1;
+    s_moved[lp] = 1;
+  }
+  __syncthreads();
+  // the other outputs of class h in ascending t, into column h's bins outside its reserved range [lo, hi)
+  const bool rem = act && !s_moved[tid];
+  int rr = 0, lo = 0, hi = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    int tot;
+    const int r = block_rank(rem && h == c, wsum, &tot);
+    if (h == c) {
+      rr = r;
+      if (e[c] > 0) { lo = min(Eb[c], G); hi = min(Eb[c] + e[c], G); }
+      else if (sp[c] > 0) { lo = min(Sb[c], E); hi = min(Sb[c] + sp[c], E); }
+    }
+  }
+  const int bin = rr < lo ? rr : rr + (hi - lo);
+  const bool ovf = rem && bin >= G;
+  if (rem && !ovf) s_lst[h][bin] = tid;
+  int novf = 0;
+  const int orank = block_rank(ovf, wsum, &novf);   // (its barriers publish s_lst)
+  if (ovf) s_over[orank] = tid;
   const bool sact = tid < d_pad;
   const int og = tid / tpo, kk = tid - og * tpo, want = og & 3, mi = (og >> 2) * tpo + kk;
-  int want_n = 0;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) want_n = (c == want) ? ncls[c] : want_n;
-  const bool over = sact && mi >= want_n;
-  int nover = 0;
-  const int orank = block_rank(over, wsum, &nover);   // (its barriers publish s_left)
-  if (sact) perm[tid] = !over ? s_lst[want][mi] : (orank < nleft ? s_left[orank] : -1);
+  const int sv = sact ? s_lst[want][mi] : -1;
+  const bool empty = sact && sv < 0;
+  int nemp = 0;
+  const int erank = block_rank(empty, wsum, &nemp);   // (its barriers publish s_over)
+  if (sact) perm[tid] = empty ? (erank < novf ? s_over[erank] : -1) : sv;
 }
 
 // Chunk signs of the sketch's gather: sgn[c][s] = (-1)^popc(c & a_t), t = perm[s], a_t = S_t / B; 0 for empty slots.
