@@ -125,6 +125,12 @@ def blocks_for(cfg, world):
 
 
 def make_config(name, cfg, world):
+    if cfg.get("planted"):
+        return {"workload": name, "n": cfg["n"], "d": cfg["d"],
+                "kernel": "stored K = E D E^T (PAPER.md:388), d_ii = exp(-0.01 i), read from HBM",
+                "omega": ["srht", "gauss", "hartley", "cosine"][cfg["omega"]], "blocks_per_gpu": blocks_for(cfg, world),
+                "m": cfg["m"], "parallelism": f"rows x{world}",
+                "l2": "flushed (256 MiB write) before every timed step"}
     return {"workload": name, "n": cfg["n"], "d": cfg["d"], "dim": cfg["dim"],
             "kernel": "sqexp" if cfg["kernel"] == 0 else "matern32",
             "omega": ["srht", "gauss", "hartley", "cosine"][cfg["omega"]], "blocks_per_gpu": blocks_for(cfg, world),
@@ -139,11 +145,12 @@ class OracleStep:
     that r x d sample -- all linear in the number of rows, so their time is scaled by n / r --
     plus the truncated back substitution and the full X = Omega Z once."""
 
-    def __init__(self, cfg, pts, A, budget_s=6.0, rows_hint=0):
+    def __init__(self, cfg, pts, A, budget_s=6.0, rows_hint=0, krows=None):
         import oracle
         self.oracle = oracle
         self.cfg = cfg
-        self.prob = oracle.Problem.from_cfg(cfg, pts)
+        self.krows = krows   # planted (stored K): rows -> K[rows] fp64 on the host
+        self.prob = oracle.Problem.from_cfg(cfg, pts if pts is not None else np.zeros((1, cfg["n"]), np.float32))
         _ = self.prob.s, self.prob.S  # randomness (setup, excluded like the GPU's)
         if cfg["omega"] == 1:
             _ = self.prob.om16
@@ -154,7 +161,7 @@ class OracleStep:
         else:  # calibrate the sketch on a small sample, then size the sample to ~budget_s
             probe = max(self.threads, 8)
             t0 = time.perf_counter()
-            self.prob.sketch_rows(np.arange(probe, dtype=np.int64))
+            self._sketch(np.arange(probe, dtype=np.int64))
             dt = time.perf_counter() - t0
             rows = int(max(probe, min(n, probe * budget_s / max(dt, 1e-3))))
         self.rows = int(min(n, max(rows, d)))
@@ -164,10 +171,15 @@ class OracleStep:
                        f"TSQR with explicit Q and Q^T A of that {self.rows}x{d} sample, times n/{self.rows}; "
                        f"truncated back substitution and the full X = Omega Z once")
 
+    def _sketch(self, rows):
+        if self.krows is not None:
+            return self.prob.sketch_stored(self.krows(rows))
+        return self.prob.sketch_rows(rows)
+
     def run(self):
         o, n = self.oracle, self.cfg["n"]
         t0 = time.perf_counter()
-        Y = self.prob.sketch_rows(self.sel)
+        Y = self._sketch(self.sel)
         Q, R = o.tsqr_tree(Y, max(1, min(self.threads, self.rows // (2 * self.cfg['d']))), want_q=True)
         Cm = o.matmul(np.ascontiguousarray(Q.T), self.A[self.sel])
         t_lin = time.perf_counter() - t0
@@ -183,11 +195,20 @@ class OracleStep:
         return c["n"] * c["n"] * c["d"] / seconds
 
 
+def planted_rows_fn(cfg):
+    """Host rows of the planted K (the device generator's K, copied back row by row)."""
+    import torch
+    from ks_inputs.planted import planted_K_device
+    K = planted_K_device(cfg["n"], cfg["seed"], torch.device("cuda", 0), **cfg["planted"])
+    return lambda rows: K[torch.as_tensor(rows, device=K.device)][:, :cfg["n"]].double().cpu().numpy()
+
+
 def run_reference(args, cfg, pts, A):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    st = OracleStep(cfg, pts, A, rows_hint=args.cpu_rows)
+    st = OracleStep(cfg, pts, A, rows_hint=args.cpu_rows,
+                    krows=planted_rows_fn(cfg) if cfg.get("planted") else None)
     for _ in range(max(0, min(args.warmup, 1))):
         st.run()
     times = [st.run() for _ in range(args.steps)]
@@ -222,7 +243,12 @@ def run_ours(args, cfg, pts_np, A_np):
     desc = dict(n=n, dim=cfg["dim"], kernel=cfg["kernel"], sigma2=cfg["sigma2"], ell=cfg["ell"],
                 nugget=cfg["nugget"], d=d, seed=cfg["seed"], omega=cfg["omega"])
     ops = ksd.CudaOps(desc, m, blocks, 1e-5, rank, world, dev)
-    pts = torch.as_tensor(pts_np, device=dev)
+    planted = bool(cfg.get("planted"))
+    if planted:   # NEXT-2: this rank's rows of the stored K = E D E^T (generated once, outside the timing)
+        from ks_inputs.planted import planted_K_device
+        pts = planted_K_device(n, cfg["seed"], dev, row_begin=rb, row_end=re, **cfg["planted"])
+    else:
+        pts = torch.as_tensor(pts_np, device=dev)
     A_loc = torch.as_tensor(np.ascontiguousarray(A_np[rb:re]), device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -302,8 +328,11 @@ def run_ours(args, cfg, pts_np, A_np):
 
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
-    if not args.no_e2e:
-        pts_h = torch.as_tensor(pts_np).pin_memory()
+    if planted and n > 10000:
+        e2e = {"value": None, "unit": "n^2*d/s", "skipped": "stored K above 10000^2: the host copy of K "
+               "(4 n^2 bytes per step) is not staged in pinned memory"}
+    elif not args.no_e2e:
+        pts_h = (pts.cpu() if planted else torch.as_tensor(pts_np)).pin_memory()
         A_h = torch.as_tensor(np.ascontiguousarray(A_np[rb:re])).pin_memory()
         X_h = torch.empty((re - rb, m), dtype=torch.float32).pin_memory()
         pts_d = torch.empty_like(pts)
@@ -336,7 +365,18 @@ def run_ours(args, cfg, pts_np, A_np):
         sm_max = float(peaks.get("sm_max_mhz", FALLBACK_SM_MHZ))
         rows_per_gpu = re - rb
         units = rows_per_gpu * n  # K elements per sketch launch on this rank
-        if cfg["omega"] == ks_inputs.OMEGA_SRHT:
+        if planted:   # the stored-K sketch streams K from HBM once: bytes / time against the copy bandwidth
+            kbytes = units * 4.0
+            achieved = kbytes / (t_sk * 1e-3) / 1e9
+            peak = float(peaks.get("hbm_gbs", 7700.0))
+            nmma = 2 if cfg["omega"] == ks_inputs.OMEGA_GAUSS else (3 if cfg["omega"] != ks_inputs.OMEGA_SRHT else 0)
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": "k_sketch_srht" if cfg["omega"] == ks_inputs.OMEGA_SRHT
+                    else "k_sketch_gauss2", "bytes_per_element": 4,
+                    "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+            if nmma:
+                roof["tensor_frac"] = 2.0 * units * d * nmma / (t_sk * 1e-3) / 1e12 / float(peaks.get("bf16_tflops", 1590.0))
+        elif cfg["omega"] == ks_inputs.OMEGA_SRHT:
             ops_elem = alu_ops_per_element(cfg)
             achieved = units * ops_elem / (t_sk * 1e-3) / 1e12
             peak = 148 * 128 * sm_max * 1e6 / 1e12
@@ -361,7 +401,9 @@ def run_ours(args, cfg, pts_np, A_np):
             roof["traffic_source"] = f"{os.path.relpath(TRAFFIC_PATH, ROOT)} ({tr['kernel']})"
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            st = OracleStep(cfg, pts_np, A_np, rows_hint=args.cpu_rows)
+            krows = (lambda rows: pts[torch.as_tensor(rows, device=dev) - rb][:, :n].double().cpu().numpy()) \
+                if planted else None
+            st = OracleStep(cfg, pts_np, A_np, rows_hint=args.cpu_rows, krows=krows)
             t_or = st.run()
             cpu = {"value": st.value(t_or), "unit": UNIT, "cores": st.threads, "kind": "oracle",
                    "sample": st.sample, "extrapolated_s_per_step": t_or}
@@ -369,7 +411,9 @@ def run_ours(args, cfg, pts_np, A_np):
             "metric": METRIC,
             "value": n * n * d / (t_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (ks_inputs, Philox seeded)",
+            "vs_baseline": None, "dtype": "f32",
+            "data": ("synthetic (planted K = E D E^T, ks_inputs.planted device generator, seeded)" if planted
+                     else "synthetic (ks_inputs, Philox seeded)"),
             "config": make_config(args.config, cfg, world),
             "sketch_n2d_per_s": n * rows_per_gpu * d * world / (t_sk * 1e-3),
             "sketch_ms": t_sk, "solve_ms": t_step, "phase_ms": ph,
@@ -386,7 +430,7 @@ def main():
     args = parse()
     cfg = dict(ks_inputs.CONFIGS[args.config])
     cfg["seed"] = ks_inputs.config_seed(args.config)
-    pts = ks_inputs.points(cfg["seed"], cfg["n"], cfg["dim"], cfg["dist"])
+    pts = None if cfg.get("planted") else ks_inputs.points(cfg["seed"], cfg["n"], cfg["dim"], cfg["dist"])
     A = ks_inputs.rhs(cfg["seed"], cfg["n"], cfg["m"])
     if args.impl == "reference":
         run_reference(args, cfg, pts, A)

@@ -57,7 +57,9 @@ typedef enum ks_status {
  * by direct differences (reading L10).
  *   KS_KERNEL_SQEXP    k = sigma2 * exp(-r^2 / (2 ell^2))               (L7)
  *   KS_KERNEL_MATERN32 k = sigma2 * (1 + sqrt3 r/ell) exp(-sqrt3 r/ell) (L8) */
-typedef enum ks_kernel_kind { KS_KERNEL_SQEXP = 0, KS_KERNEL_MATERN32 = 1 } ks_kernel_kind;
+/*   KS_KERNEL_STORED   K is not generated: ks_sketch_stored reads it from device memory (NEXT-2, the
+ *                      planted-spectrum workload K = E D E^T of PAPER.md:388); valid only there. */
+typedef enum ks_kernel_kind { KS_KERNEL_SQEXP = 0, KS_KERNEL_MATERN32 = 1, KS_KERNEL_STORED = 2 } ks_kernel_kind;
 
 /* Random projection Omega (n x d):
  *   KS_OMEGA_SRHT  Def. 1, T = Walsh-Hadamard (:74-89):
@@ -102,6 +104,21 @@ KS_API ks_status ks_sketch_workspace_size(const ks_sketch_desc* desc, size_t* by
  * kernel limits), CUDA. */
 KS_API ks_status ks_sketch(const ks_sketch_desc* desc, const float* pts_dev, int64_t row_begin, int64_t row_end,
                     float* Y_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+
+/* NEXT-2: Y = rows [row_begin, row_end) of K Omega for a STORED K (PAPER.md:95 with the planted-spectrum
+ * K = E D E^T of PAPER.md:388 "we start therefore with a known spectral decomposition"): the same Omega,
+ * randomness and workspace as ks_sketch, but the sketch kernels stream K from HBM instead of evaluating
+ * the covariance (an HBM-bound ingest of n^2 * 4 bytes).
+ *   K_dev : device, fp32, row-major: rows [row_begin, row_end) of K, K[i][j] at K_dev[(i - row_begin) * ldk + j]
+ *           (a rank passes just its row block); ldk >= n, ldk % 4 == 0, 16-byte aligned.  Columns [0, n)
+ *           are read.  Not modified.
+ *   desc  : kernel must be KS_KERNEL_STORED; dim and ell are ignored; sigma2 must bound max |K_ij| (it
+ *           sets the fp16 scaling of the GAUSS / DHT / DCT tensor-core path; K itself is used unscaled);
+ *           nugget is added to the diagonal by index as in ks_sketch (use 0 for K = E D E^T).
+ * Errors: as ks_sketch; INVALID_ARGUMENT also for kernel != KS_KERNEL_STORED, ldk < n, ldk % 4 != 0 or a
+ * misaligned K_dev. */
+KS_API ks_status ks_sketch_stored(const ks_sketch_desc* desc, const float* K_dev, int64_t ldk, int64_t row_begin,
+                                  int64_t row_end, float* Y_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
 
 /* Export the sketch randomness for bit-exact tests (device outputs; any may be NULL):
  *   signs_dev  int8[N]       s_j in {-1,+1}      (Def. 1 "Rademacher")

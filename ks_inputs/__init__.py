@@ -130,7 +130,16 @@ CONFIGS = {
 # cosine ("HC") structured projections (Table 3).
 CONFIGS["c3h"] = dict(CONFIGS["c3"], omega=OMEGA_DHT)
 CONFIGS["c3c"] = dict(CONFIGS["c3"], omega=OMEGA_DCT)
-CONFIG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5, "c3h": 3, "c3c": 3}
+# NEXT-2: the planted-spectrum workload: K = E D E^T stored in HBM (ks_inputs.planted), the
+# paper's Gaussian Omega (and its Hartley / cosine variants at n = 50000), d = 256, sketched from the stored K.
+for _n, _tag, _b in ((1000, "1k", 1), (5000, "5k", 2), (10000, "10k", 4), (50000, "50k", 8)):
+    CONFIGS["p" + _tag] = dict(n=_n, dim=1, dist="planted", kernel=2, sigma2=1.0, ell=1.0, nugget=0.0, d=256,
+                               omega=OMEGA_GAUSS, blocks=_b, m=16, planted=dict(scale=1.0, rate=0.01))
+CONFIGS["p50kh"] = dict(CONFIGS["p50k"], omega=OMEGA_DHT)
+CONFIGS["p50kc"] = dict(CONFIGS["p50k"], omega=OMEGA_DCT)
+CONFIGS["p50ks"] = dict(CONFIGS["p50k"], omega=OMEGA_SRHT)
+CONFIG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5, "c3h": 3, "c3c": 3,
+                "p1k": 11, "p5k": 12, "p10k": 13, "p50k": 14, "p50kh": 14, "p50kc": 14, "p50ks": 14}
 
 
 def config_seed(name: str) -> int:
@@ -145,6 +154,6 @@ def make_problem(name: str | None = None, *, seed: int | None = None, **override
     if seed is None:
         seed = config_seed(name) if name else 1
     cfg["seed"] = int(seed)
-    pts = points(cfg["seed"], cfg["n"], cfg["dim"], cfg.get("dist", "uniform"))
+    pts = None if cfg.get("planted") else points(cfg["seed"], cfg["n"], cfg["dim"], cfg.get("dist", "uniform"))
     A = rhs(cfg["seed"], cfg["n"], cfg["m"])
     return cfg, pts, A

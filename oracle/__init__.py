@@ -273,6 +273,11 @@ class Problem:
                                    _p(om), self.d, _p(rows), rows.shape[0], _p(Y), _threads(nthreads))
         return Y
 
+    def sketch_stored(self, K_rows: np.ndarray) -> np.ndarray:
+        """NEXT-2: rows of Y = K Omega for a stored K (PAPER.md:95 with K = E D E^T of :388): the given rows
+        of K (r x n) times the explicit Omega, one library matmul (fp64)."""
+        return matmul(np.ascontiguousarray(K_rows, np.float64), self.omega_dense())
+
     def omega_apply(self, Z: np.ndarray) -> np.ndarray:
         Z = np.ascontiguousarray(Z, np.float64)
         m = Z.shape[1]

@@ -18,7 +18,7 @@ import os
 import torch
 
 __all__ = [
-    "KsError", "SketchDesc", "SQEXP", "MATERN32", "SRHT", "GAUSS", "DHT", "DCT", "lib", "library_path",
+    "KsError", "SketchDesc", "SQEXP", "MATERN32", "STORED", "ks_sketch_stored", "SRHT", "GAUSS", "DHT", "DCT", "lib", "library_path",
     "ks_sketch_workspace_size", "ks_sketch", "ks_omega_export", "ks_omega_apply",
     "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr", "ks_qform", "TSQR_TREE", "TSQR_CHAIN",
     "ks_tsqr_workspace_size_ex", "ks_tsqr_create_ex", "ks_tsqr_apply_qt", "ks_tsqr_apply_q",
@@ -30,7 +30,7 @@ __all__ = [
 _HERE = os.path.dirname(os.path.abspath(__file__))
 library_path = os.path.join(_HERE, "libks_b200.so")
 
-SQEXP, MATERN32 = 0, 1
+SQEXP, MATERN32, STORED = 0, 1, 2   # ks_kernel_kind (STORED: NEXT-2, K read from device memory)
 SRHT, GAUSS, DHT, DCT = 0, 1, 2, 3   # ks_omega_kind (DHT / DCT: NEXT-1 structured Hartley / cosine)
 STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARGUMENT", 2: "KS_ERR_SINGULAR", 3: "KS_ERR_CUDA", 4: "KS_ERR_OOM",
           5: "KS_ERR_UNSUPPORTED", 6: "KS_ERR_NCCL"}
@@ -58,6 +58,7 @@ _P, _i64, _i32, _f32, _sz = C.c_void_p, C.c_int64, C.c_int32, C.c_float, C.c_siz
 _SIGS = {
     "ks_sketch_workspace_size": [C.POINTER(SketchDesc), C.POINTER(_sz)],
     "ks_sketch": [C.POINTER(SketchDesc), _P, _i64, _i64, _P, _P, _sz, _P],
+    "ks_sketch_stored": [C.POINTER(SketchDesc), _P, _i64, _i64, _i64, _P, _P, _sz, _P],
     "ks_omega_export": [C.POINTER(SketchDesc), _P, _P, _P, _P, _sz, _P],
     "ks_omega_apply": [C.POINTER(SketchDesc), _P, _i32, _i64, _i64, _P, _P, _sz, _P],
     "ks_tsqr_workspace_size": [_i64, _i32, _i32, C.POINTER(_sz)],
@@ -148,6 +149,12 @@ def ks_sketch(desc, pts, row_begin, row_end, Y, ws, stream=None):
     _check(lib().ks_sketch(C.byref(_desc(desc)), _ptr(pts, torch.float32, "pts"), int(row_begin), int(row_end),
                            _ptr(Y, torch.float32, "Y"), _ptr(ws, None, "ws"), ws.numel() * ws.element_size(),
                            _stream(stream)))
+
+
+def ks_sketch_stored(desc, K, ldk, row_begin, row_end, Y, ws, stream=None):
+    _check(lib().ks_sketch_stored(C.byref(_desc(desc)), _ptr(K, torch.float32, "K"), int(ldk), int(row_begin),
+                                  int(row_end), _ptr(Y, torch.float32, "Y"), _ptr(ws, None, "ws"),
+                                  ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def ks_omega_export(desc, signs, sel, gauss, ws, stream=None):
@@ -277,6 +284,16 @@ class Sketch:
         if Y is None:
             Y = torch.empty((row_end - row_begin, d), dtype=torch.float32, device=self.device)
         ks_sketch(self.desc, pts, row_begin, row_end, Y, self.ws, stream)
+        return Y
+
+    def stored(self, K, row_begin=0, row_end=None, Y=None, stream=None):
+        """Y = rows [row_begin, row_end) of K Omega for a stored K: K holds those rows, (rows x ldk) fp32 on
+        the device (NEXT-2)."""
+        n, d = self.desc.n, self.desc.d
+        row_end = n if row_end is None else row_end
+        if Y is None:
+            Y = torch.empty((row_end - row_begin, d), dtype=torch.float32, device=self.device)
+        ks_sketch_stored(self.desc, K, K.stride(0), row_begin, row_end, Y, self.ws, stream)
         return Y
 
     def omega_apply(self, Z, row_begin=0, row_end=None, X=None, stream=None):

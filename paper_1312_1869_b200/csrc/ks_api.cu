@@ -59,6 +59,25 @@ extern "C" ks_status ks_sketch(const ks_sketch_desc* desc, const float* pts, int
   KS_GUARD_END
 }
 
+extern "C" ks_status ks_sketch_stored(const ks_sketch_desc* desc, const float* K, int64_t ldk, int64_t rb, int64_t re,
+                                      float* Y, void* ws, size_t ws_bytes, ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  if (!desc) return fail(KS_ERR_INVALID_ARGUMENT, "desc is NULL");
+  if (desc->kernel != KS_KERNEL_STORED) return fail(KS_ERR_INVALID_ARGUMENT, "ks_sketch_stored needs KS_KERNEL_STORED");
+  KS_TRY(sketch_validate(desc));
+  KS_TRY(check_rows(desc, rb, re));
+  if (!K || !ws || (re > rb && !Y)) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if (ldk < desc->n || (ldk & 3) != 0 || (reinterpret_cast<uintptr_t>(K) & 15) != 0)
+    return fail(KS_ERR_INVALID_ARGUMENT, "need ldk >= n, ldk % 4 == 0 and a 16-byte aligned K");
+  const SketchLayout L = sketch_layout(*desc);
+  if (ws_bytes < L.bytes) return fail(KS_ERR_OOM, "sketch workspace too small: need " + std::to_string(L.bytes));
+  char* w = static_cast<char*>(ws);
+  KS_TRY(sketch_prepare(*desc, L, nullptr, w, S(stream), true));
+  const StoredK sk{K, ldk};
+  return sketch_run(*desc, L, rb, re, Y, w, S(stream), &sk);
+  KS_GUARD_END
+}
+
 extern "C" ks_status ks_omega_export(const ks_sketch_desc* desc, int8_t* signs, int32_t* sel, uint16_t* gauss,
                                      void* ws, size_t ws_bytes, ks_stream_t stream) {
   KS_GUARD_BEGIN

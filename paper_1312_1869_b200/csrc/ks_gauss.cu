@@ -85,6 +85,60 @@ KS_DEVINL void produce_tile(const f2_t (&xi2)[2][3], const int64_t (&irow)[4], c
   }
 }
 
+// Stored K (NEXT-2): the same tile from K in HBM, v = K[i][j] * a_j (a_j = S), no evaluation.
+KS_DEVINL void produce_tile_stored(const float* __restrict__ Kst, int64_t ldk, int64_t ncols,
+                                   const int64_t (&irow)[4], int64_t row_last, const float4 (&pts)[8], int64_t j0,
+                                   bool diag, float nugget, uint8_t* a_hi, uint8_t* a_lo, int rq, int cq) {
+  float kv[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float* kr = Kst + (irow[r] <= row_last ? irow[r] : row_last) * ldk + j0;
+    if (j0 + 8 <= ncols) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(kr)), b = __ldg(reinterpret_cast<const float4*>(kr + 4));
+      kv[r][0] = a.x; kv[r][1] = a.y; kv[r][2] = a.z; kv[r][3] = a.w;
+      kv[r][4] = b.x; kv[r][5] = b.y; kv[r][6] = b.z; kv[r][7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) kv[r][q] = j0 + q < ncols ? __ldg(kr + q) : 0.f;
+    }
+  }
+#pragma unroll
+  for (int pr = 0; pr < 2; ++pr) {
+    f2_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = f2mul(f2(kv[2 * pr][q], kv[2 * pr + 1][q]), f2s(pts[q].w));
+    if (diag) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float a = f2lo(v[q]), b = f2hi(v[q]);
+        if (j0 + q == irow[2 * pr]) a += nugget;
+        if (j0 + q == irow[2 * pr + 1]) b += nugget;
+        v[q] = f2(a, b);
+      }
+    }
+    uint32_t hi[2][4], lo[2][4];
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      const f2_t h0 = f2(__uint_as_float(__float_as_uint(f2lo(v[q])) & 0xFFFFE000u),
+                         __uint_as_float(__float_as_uint(f2hi(v[q])) & 0xFFFFE000u));
+      const f2_t h1 = f2(__uint_as_float(__float_as_uint(f2lo(v[q + 1])) & 0xFFFFE000u),
+                         __uint_as_float(__float_as_uint(f2hi(v[q + 1])) & 0xFFFFE000u));
+      const f2_t l0 = f2sub(v[q], h0), l1 = f2sub(v[q + 1], h1);
+      hi[0][q >> 1] = pack_half2(f2lo(h0), f2lo(h1));
+      hi[1][q >> 1] = pack_half2(f2hi(h0), f2hi(h1));
+      lo[0][q >> 1] = pack_half2(f2lo(l0), f2lo(l1));
+      lo[1][q >> 1] = pack_half2(f2hi(l0), f2hi(l1));
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 4 * rq + 2 * pr + h;
+      const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
+      sts128(smem_u32(a_hi + off), hi[h][0], hi[h][1], hi[h][2], hi[h][3]);
+      sts128(smem_u32(a_lo + off), lo[h][0], lo[h][1], lo[h][2], lo[h][3]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ 2-CTA kernel (cta_group::2)
 // A CTA pair (cluster of 2, same TPC) computes a 256-row tile with M = 256 MMAs issued by the leader:
 // each CTA supplies its own 128 rows of K (A operand, produced in its smem) and HALF of Omega^T
@@ -151,7 +205,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGThreads, 1)
 k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmP,
                 const float4* __restrict__ pk, int64_t row_begin,
                 int64_t row_end, int nkb_all, int seg_kb, int DN, float nugget, float out_scale,
-                float* __restrict__ Y0, float* __restrict__ Y1, int dbg) {
+                float* __restrict__ Y0, float* __restrict__ Y1, int dbg, const float* __restrict__ Kst, int64_t ldk,
+                int64_t ncols) {
   // split-K: blockIdx.y selects the half of the column blocks (Y0 gets the first half's partial sum,
   // Y1 the second's; k_add_halves adds them) so that the row tiles fill a whole number of waves.
   const int kh = blockIdx.y, nkb_a = gridDim.y > 1 ? nkb_all / 2 : nkb_all;
@@ -307,7 +362,10 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       if (lane == 0) mbar_arrive(pempty0 + 8 * ps);   // release: this warp's reads of the slot are done
       mbar_wait(empty0 + 8 * s, ph ^ 1);
       const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
-      if (!(dbg & 2))   // bit 1 skips the producers' arithmetic
+      if constexpr (KIND == KS_KERNEL_STORED)
+        produce_tile_stored(Kst - row_begin * ldk, ldk, ncols, irow, row_end - 1, pts, j0, diag, nugget, a_hi + s * kATileBytes,
+                            a_lo + s * kATileBytes, rq, cq);
+      else if (!(dbg & 2))   // bit 1 skips the producers' arithmetic
         produce_tile<DIM, KIND>(xi2, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
       fence_proxy_async();
       __syncwarp();
@@ -401,7 +459,7 @@ static int gauss_seg_kb() {
 
 template <int DIM, int KIND, int NB>
 static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
-                              char* ws, cudaStream_t st) {
+                              char* ws, cudaStream_t st, const StoredK* sk) {
   auto encode = get_encode();
   if (!encode) return fail(KS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int DN = D.d;
@@ -446,7 +504,8 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   static const int dbg = [] { const char* e = getenv("KS_GAUSS_DEBUG"); return e ? atoi(e) : 0; }();
   // NB = 2 issues 3 MMAs per K step: 11 stages per segment keep the non-RN accumulation run as for NB = 1
   const int seg = NB == 1 ? gauss_seg_kb() : std::max(1, gauss_seg_kb() * 2 / 3);
-  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, seg, DN, nug, osc, Y, Y1, dbg);
+  kern<<<grid, kGThreads, smem, st>>>(tm2, tmP, pk, rb, re, nkb, seg, DN, nug, osc, Y, Y1, dbg, sk ? sk->K : nullptr,
+                                      sk ? sk->ldk : 0, D.n);
   KS_LAUNCH_CHECK();
   if (ksplit == 2) {
     const int64_t tot = (re - rb) * (int64_t)DN;
@@ -459,13 +518,14 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
 
 template <int DIM, int KIND>
 static ks_status launch_gauss_nb(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
-                                 char* ws, cudaStream_t st) {
-  return D.omega == KS_OMEGA_GAUSS ? launch_gauss<DIM, KIND, 1>(D, L, rb, re, Y, ws, st)
-                                   : launch_gauss<DIM, KIND, 2>(D, L, rb, re, Y, ws, st);
+                                 char* ws, cudaStream_t st, const StoredK* sk = nullptr) {
+  return D.omega == KS_OMEGA_GAUSS ? launch_gauss<DIM, KIND, 1>(D, L, rb, re, Y, ws, st, sk)
+                                   : launch_gauss<DIM, KIND, 2>(D, L, rb, re, Y, ws, st, sk);
 }
 
 ks_status gauss_sketch_run(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y,
-                           char* ws, cudaStream_t st) {
+                           char* ws, cudaStream_t st, const StoredK* sk) {
+  if (sk) return launch_gauss_nb<1, KS_KERNEL_STORED>(D, L, rb, re, Y, ws, st, sk);
   const bool se = D.kernel == KS_KERNEL_SQEXP;
   switch (D.dim) {
     case 1: return se ? launch_gauss_nb<1, KS_KERNEL_SQEXP>(D, L, rb, re, Y, ws, st)

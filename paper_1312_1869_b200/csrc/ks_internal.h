@@ -59,14 +59,19 @@ SketchLayout sketch_layout(const ks_sketch_desc& desc);
 // Fill the workspace with this desc's randomness (packed points need pts).
 ks_status sketch_prepare(const ks_sketch_desc& desc, const SketchLayout& L, const float* pts, char* ws,
                          cudaStream_t st, bool need_points);
+// A stored K (NEXT-2): row-major fp32, K[i][j] at K[i * ldk + j].
+struct StoredK {
+  const float* K;
+  int64_t ldk;
+};
 ks_status sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, int64_t row_begin, int64_t row_end,
-                     float* Y, char* ws, cudaStream_t st);
+                     float* Y, char* ws, cudaStream_t st, const StoredK* sk = nullptr);
 ks_status omega_apply_run(const ks_sketch_desc& desc, const SketchLayout& L, const float* Z, int m,
                           int64_t row_begin, int64_t row_end, float* X, char* ws, cudaStream_t st);
 ks_status omega_export_run(const ks_sketch_desc& desc, const SketchLayout& L, int8_t* signs, int32_t* sel,
                            uint16_t* gauss, char* ws, cudaStream_t st);
 ks_status gauss_sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, int64_t row_begin,
-                           int64_t row_end, float* Y, char* ws, cudaStream_t st);
+                           int64_t row_end, float* Y, char* ws, cudaStream_t st, const StoredK* sk);
 
 // ---------------------------------------------------------------- TSQR
 // Plans replay their launch sequence as a cached CUDA graph; one-shot plans switch that off.

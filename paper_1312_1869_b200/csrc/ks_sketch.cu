@@ -66,11 +66,12 @@ ks_status sketch_validate(const ks_sketch_desc* desc) {
   const ks_sketch_desc& D = *desc;
   if (D.n < 1) return fail(KS_ERR_INVALID_ARGUMENT, "n must be >= 1");
   if (D.n > (int64_t(1) << 30)) return fail(KS_ERR_UNSUPPORTED, "n > 2^30 not supported");
-  if (D.dim < 1 || D.dim > 3) return fail(KS_ERR_INVALID_ARGUMENT, "dim must be 1, 2 or 3");
-  if (D.kernel != KS_KERNEL_SQEXP && D.kernel != KS_KERNEL_MATERN32)
+  const bool stored = D.kernel == KS_KERNEL_STORED;
+  if (!stored && (D.dim < 1 || D.dim > 3)) return fail(KS_ERR_INVALID_ARGUMENT, "dim must be 1, 2 or 3");
+  if (D.kernel != KS_KERNEL_SQEXP && D.kernel != KS_KERNEL_MATERN32 && !stored)
     return fail(KS_ERR_INVALID_ARGUMENT, "unknown kernel kind");
   if (!(D.sigma2 > 0.0f) || !std::isfinite(D.sigma2)) return fail(KS_ERR_INVALID_ARGUMENT, "sigma2 must be > 0");
-  if (!(D.ell > 0.0f) || !std::isfinite(D.ell)) return fail(KS_ERR_INVALID_ARGUMENT, "ell must be > 0");
+  if (!stored && (!(D.ell > 0.0f) || !std::isfinite(D.ell))) return fail(KS_ERR_INVALID_ARGUMENT, "ell must be > 0");
   if (!(D.nugget >= 0.0f) || !std::isfinite(D.nugget)) return fail(KS_ERR_INVALID_ARGUMENT, "nugget must be >= 0");
   const int64_t N = next_pow2(D.n);
   if (D.d < 1 || D.d > N) return fail(KS_ERR_INVALID_ARGUMENT, "need 1 <= d <= N");
@@ -97,9 +98,11 @@ __global__ void k_pack_points(const float* __restrict__ pts, int64_t n, int dim,
   if (j >= ncols_pad) return;
   float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
   if (j < n) {
-    p.x = pts[j] * scale;
-    if (dim > 1) p.y = pts[n + j] * scale;
-    if (dim > 2) p.z = pts[2 * n + j] * scale;
+    if (pts) {   // (a stored K has no points: amplitudes only)
+      p.x = pts[j] * scale;
+      if (dim > 1) p.y = pts[n + j] * scale;
+      if (dim > 2) p.z = pts[2 * n + j] * scale;
+    }
     p.w = srht ? rademacher(seed, j) * sigma2 : sigma2;
   }
   pk[j] = p;
@@ -373,6 +376,7 @@ double gauss_scale(const ks_sketch_desc& D) {
 }
 
 static float coord_scale(const ks_sketch_desc& D) {
+  if (D.kernel == KS_KERNEL_STORED) return 1.f;
   if (D.kernel == KS_KERNEL_SQEXP) return (float)std::sqrt(1.4426950408889634 / (2.0 * (double)D.ell * (double)D.ell));
   return (float)(std::sqrt(3.0) / (double)D.ell);
 }
@@ -382,7 +386,9 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
   const int srht = D.omega == KS_OMEGA_SRHT;
   if (need_points) {
     const int64_t nb = (L.ncols_pad + 255) / 256;
-    const float amp = srht ? D.sigma2 : (float)(D.sigma2 * gauss_scale(D));
+    // a stored K carries its own scale: amplitude s_j (SRHT) or S (tensor-core path)
+    const float sig = D.kernel == KS_KERNEL_STORED ? 1.f : D.sigma2;
+    const float amp = srht ? sig : (float)(sig * gauss_scale(D));
     k_pack_points<<<(unsigned)nb, 256, 0, st>>>(pts, D.n, D.dim, L.ncols_pad, coord_scale(D), amp, D.seed,
                                                  srht, reinterpret_cast<float4*>(ws + L.off_pk));
     KS_LAUNCH_CHECK();
@@ -459,7 +465,8 @@ template <int DIM, int KIND, int TPO>
 __global__ void __launch_bounds__(kSrhtThreads, 4)
 k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, const int32_t* __restrict__ perm,
               const float* __restrict__ sgn, int64_t row_begin, int64_t row_end, int A, int d, int d_pad,
-              float out_scale, float nugget, float* __restrict__ Y) {
+              float out_scale, float nugget, float* __restrict__ Y, const float* __restrict__ Kst, int64_t ldk,
+              int64_t ncols) {
   extern __shared__ __align__(16) float Wbuf[];   // [2][kSrhtSmemFloats], chunk c uses half c & 1
   float4* Pbuf = reinterpret_cast<float4*>(Wbuf + 2 * kSrhtSmemFloats);   // [2][kSrhtB] packed points
   const int t = threadIdx.x;
@@ -471,12 +478,14 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
   const int oB = 264 * g + rp;             // + 8 b     (= srht_w(32 g + b, rp))
 
   f2_t xi2[3];
+  const float *kr0 = nullptr, *kr1 = nullptr;   // stored K (NEXT-2): this thread's two rows
   {
     int64_t i0 = row0 + 2 * rg, i1 = i0 + 1;
     if (i0 >= row_end) i0 = row_end - 1;
     if (i1 >= row_end) i1 = row_end - 1;
     const float4 a = pk[i0], b = pk[i1];
     xi2[0] = f2(a.x, b.x); xi2[1] = f2(a.y, b.y); xi2[2] = f2(a.z, b.z);
+    if (KIND == KS_KERNEL_STORED) { kr0 = Kst + (i0 - row_begin) * ldk; kr1 = Kst + (i1 - row_begin) * ldk; }
   }
   int wofs[TPO];
 #pragma unroll
@@ -507,6 +516,21 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
     {
       const float4* pc = Pbuf + (c & 1) * kSrhtB + cg;
       f2_t v[16];
+      if constexpr (KIND == KS_KERNEL_STORED) {   // K streamed from HBM: all 32 loads issued up front
+        const int64_t jb = (int64_t)c * kSrhtB + cg;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t j = jb + 32 * q;
+          v[q] = j < ncols ? f2(__ldg(kr0 + j), __ldg(kr1 + j)) : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {   // level h = 1 with the signs a_j = s_j folded in
+          const float4 p0 = pc[32 * q], p1 = pc[32 * (q + 1)];
+          const f2_t m0 = f2mul(v[q], f2s(p0.w)), k1 = v[q + 1];
+          v[q] = f2fma(k1, f2s(p1.w), m0);
+          v[q + 1] = f2fma(k1, f2s(-p1.w), m0);
+        }
+      } else {
 #pragma unroll
       for (int q = 0; q < 16; q += 2) {   // level h = 1 with the amplitudes a_j = s_j sigma^2 folded in
         const float4 p0 = pc[32 * q], p1 = pc[32 * (q + 1)];
@@ -514,6 +538,7 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
         const f2_t m0 = f2mul(k0, f2s(p0.w));
         v[q] = f2fma(k1, f2s(p1.w), m0);
         v[q + 1] = f2fma(k1, f2s(-p1.w), m0);
+      }
       }
 #pragma unroll
       for (int h = 2; h < 16; h <<= 1)
@@ -584,7 +609,7 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
 
 template <int DIM, int KIND, int TPO>
 static ks_status launch_srht(const SketchLayout& L, const ks_sketch_desc& D, int64_t rb, int64_t re, float* Y,
-                             char* ws, cudaStream_t st) {
+                             char* ws, cudaStream_t st, const StoredK* sk) {
   auto kern = k_sketch_srht<DIM, KIND, TPO>;
   const int smem = kSrhtSmemBytes;
   KS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -593,27 +618,29 @@ static ks_status launch_srht(const SketchLayout& L, const ks_sketch_desc& D, int
                                 reinterpret_cast<const int32_t*>(ws + L.off_sel),
                                 reinterpret_cast<const int32_t*>(ws + L.off_perm),
                                 reinterpret_cast<const float*>(ws + L.off_sgn), rb, re, L.A, D.d, L.d_pad,
-                                (float)(1.0 / std::sqrt((double)L.N)), D.nugget, Y);
+                                (float)(1.0 / std::sqrt((double)L.N)), D.nugget, Y, sk ? sk->K : nullptr,
+                                sk ? sk->ldk : 0, D.n);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }
 
 template <int DIM, int KIND>
 static ks_status dispatch_tpo(const SketchLayout& L, const ks_sketch_desc& D, int64_t rb, int64_t re, float* Y,
-                              char* ws, cudaStream_t st) {
+                              char* ws, cudaStream_t st, const StoredK* sk = nullptr) {
   switch (L.tpo) {
-    case 1: return launch_srht<DIM, KIND, 1>(L, D, rb, re, Y, ws, st);
-    case 2: return launch_srht<DIM, KIND, 2>(L, D, rb, re, Y, ws, st);
-    case 4: return launch_srht<DIM, KIND, 4>(L, D, rb, re, Y, ws, st);
-    case 8: return launch_srht<DIM, KIND, 8>(L, D, rb, re, Y, ws, st);
+    case 1: return launch_srht<DIM, KIND, 1>(L, D, rb, re, Y, ws, st, sk);
+    case 2: return launch_srht<DIM, KIND, 2>(L, D, rb, re, Y, ws, st, sk);
+    case 4: return launch_srht<DIM, KIND, 4>(L, D, rb, re, Y, ws, st, sk);
+    case 8: return launch_srht<DIM, KIND, 8>(L, D, rb, re, Y, ws, st, sk);
   }
   return fail(KS_ERR_UNSUPPORTED, "unsupported SRHT output width");
 }
 
 ks_status sketch_run(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb, int64_t re, float* Y, char* ws,
-                     cudaStream_t st) {
+                     cudaStream_t st, const StoredK* sk) {
   if (re <= rb) return KS_OK;
-  if (D.omega != KS_OMEGA_SRHT) return gauss_sketch_run(D, L, rb, re, Y, ws, st);   // Gaussian, Hartley, cosine
+  if (D.omega != KS_OMEGA_SRHT) return gauss_sketch_run(D, L, rb, re, Y, ws, st, sk);   // Gaussian, Hartley, cosine
+  if (sk) return dispatch_tpo<1, KS_KERNEL_STORED>(L, D, rb, re, Y, ws, st, sk);
   const bool se = D.kernel == KS_KERNEL_SQEXP;
   switch (D.dim) {
     case 1: return se ? dispatch_tpo<1, KS_KERNEL_SQEXP>(L, D, rb, re, Y, ws, st)

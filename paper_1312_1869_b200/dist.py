@@ -57,7 +57,12 @@ class CudaOps:
         self.qt_ws = _ws(ks_apply_qt_workspace_size(rows, d, self.m), self.device)
 
     def sketch(self, pts):
-        self._f["sketch"](self.desc, pts, self.rb, self.re, self.Y, self.sk.ws)
+        """pts: the points (dim x n), or -- KS_KERNEL_STORED (NEXT-2) -- this rank's rows of K (rows x ldk)."""
+        if self.desc.kernel == 2:
+            from . import ks_sketch_stored
+            ks_sketch_stored(self.desc, pts, pts.shape[1], self.rb, self.re, self.Y, self.sk.ws)
+        else:
+            self._f["sketch"](self.desc, pts, self.rb, self.re, self.Y, self.sk.ws)
         return self.Y
 
     def local_r(self, Y):

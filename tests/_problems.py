@@ -28,3 +28,15 @@ def align_rows(Rg, Rr):
     s = np.sign(np.sum(Rg * Rr, axis=1))
     s[s == 0] = 1
     return Rg * s[:, None]
+
+
+def planted_problem(n, d, omega, seed=77, rank=None, rate=0.01, m=8):
+    """NEXT-2: the planted-spectrum K = E D E^T (ks_inputs.planted, host generator) as the fp32 K both
+    sides read, with a problem descriptor for the stored-K sketch."""
+    from ks_inputs.planted import planted_K
+    K64, E, dvals = planted_K(n, seed, 1.0, rate, rank)
+    K = K64.astype(np.float32)
+    cfg = dict(n=n, dim=1, kernel=2, sigma2=1.0, ell=1.0, nugget=0.0, d=d, seed=seed, omega=omega, m=m)
+    prob = oracle.Problem.from_cfg(cfg, np.zeros((1, n), np.float32))
+    A = ks_inputs.rhs(seed, n, m)
+    return cfg, K, E, dvals, A, prob
