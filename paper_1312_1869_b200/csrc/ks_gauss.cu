@@ -85,11 +85,11 @@ KS_DEVINL void produce_tile(const f2_t (&xi2)[2][3], const int64_t (&irow)[4], c
   }
 }
 
-// Stored K (NEXT-2): the same tile from K in HBM, v = K[i][j] * a_j (a_j = S), no evaluation.
-KS_DEVINL void produce_tile_stored(const float* __restrict__ Kst, int64_t ldk, int64_t ncols,
-                                   const int64_t (&irow)[4], int64_t row_last, const float4 (&pts)[8], int64_t j0,
-                                   bool diag, float nugget, uint8_t* a_hi, uint8_t* a_lo, int rq, int cq) {
-  float kv[4][8];
+// Stored K (NEXT-2): the same tile from K in HBM, v = K[i][j] * a_j (a_j = S), no evaluation.  The loads
+// of the next stage are issued right after this stage's tile is stored (load_tile_stored), so they are in
+// flight while the producer waits on the ring barriers.
+KS_DEVINL void load_tile_stored(const float* __restrict__ Kst, int64_t ldk, int64_t ncols, const int64_t (&irow)[4],
+                                int64_t row_last, int64_t j0, float (&kv)[4][8]) {
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const float* kr = Kst + (irow[r] <= row_last ? irow[r] : row_last) * ldk + j0;
@@ -102,6 +102,9 @@ KS_DEVINL void produce_tile_stored(const float* __restrict__ Kst, int64_t ldk, i
       for (int q = 0; q < 8; ++q) kv[r][q] = j0 + q < ncols ? __ldg(kr + q) : 0.f;
     }
   }
+}
+KS_DEVINL void produce_tile_stored(const float (&kv)[4][8], const int64_t (&irow)[4], const float4 (&pts)[8],
+                                   int64_t j0, bool diag, float nugget, uint8_t* a_hi, uint8_t* a_lo, int rq, int cq) {
 #pragma unroll
   for (int pr = 0; pr < 2; ++pr) {
     f2_t v[8];
@@ -349,6 +352,9 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       }
       xi2[pr][0] = f2(q[0].x, q[1].x); xi2[pr][1] = f2(q[0].y, q[1].y); xi2[pr][2] = f2(q[0].z, q[1].z);
     }
+    const float* Kb = Kst - row_begin * ldk;   // (stored K: row i at Kb + i * ldk)
+    float kv[4][8];
+    if constexpr (KIND == KS_KERNEL_STORED) load_tile_stored(Kb, ldk, ncols, irow, row_end - 1, (int64_t)kb0 * kGaussBK + 8 * cq, kv);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % NST;
       const uint32_t ph = (kb / NST) & 1;
@@ -362,10 +368,10 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       if (lane == 0) mbar_arrive(pempty0 + 8 * ps);   // release: this warp's reads of the slot are done
       mbar_wait(empty0 + 8 * s, ph ^ 1);
       const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
-      if constexpr (KIND == KS_KERNEL_STORED)
-        produce_tile_stored(Kst - row_begin * ldk, ldk, ncols, irow, row_end - 1, pts, j0, diag, nugget, a_hi + s * kATileBytes,
-                            a_lo + s * kATileBytes, rq, cq);
-      else if (!(dbg & 2))   // bit 1 skips the producers' arithmetic
+      if constexpr (KIND == KS_KERNEL_STORED) {
+        produce_tile_stored(kv, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
+        if (kb + 1 < nkb) load_tile_stored(Kb, ldk, ncols, irow, row_end - 1, j0 + kGaussBK, kv);
+      } else if (!(dbg & 2))   // bit 1 skips the producers' arithmetic
         produce_tile<DIM, KIND>(xi2, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
       fence_proxy_async();
       __syncwarp();

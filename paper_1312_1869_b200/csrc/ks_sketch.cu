@@ -461,6 +461,15 @@ KS_DEVINL void cp_async16(void* smem_dst, const void* gmem_src) {
 KS_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 KS_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// Stored K: this thread's 32 values of a chunk (rows i0, i1 packed; columns jb + 32 q), zero beyond n.
+KS_DEVINL void load_k32(f2_t (&kv)[16], const float* kr0, const float* kr1, int64_t jb, int64_t ncols) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int64_t j = jb + 32 * q;
+    kv[q] = j < ncols ? f2(__ldg(kr0 + j), __ldg(kr1 + j)) : 0ull;
+  }
+}
+
 template <int DIM, int KIND, int TPO>
 __global__ void __launch_bounds__(kSrhtThreads, 4)
 k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, const int32_t* __restrict__ perm,
@@ -493,6 +502,8 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
     const int tt = perm[og * TPO + k];
     wofs[k] = srht_w(tt >= 0 ? (sel[tt] & (kSrhtB - 1)) : 0, 4 * rq);
   }
+  f2_t kpre[KIND == KS_KERNEL_STORED ? 16 : 1];
+  if constexpr (KIND == KS_KERNEL_STORED) load_k32(kpre, kr0, kr1, cg, ncols);
   f2_t acc[TPO][2];
 #pragma unroll
   for (int k = 0; k < TPO; ++k) acc[k][0] = acc[k][1] = 0ull;
@@ -516,13 +527,9 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
     {
       const float4* pc = Pbuf + (c & 1) * kSrhtB + cg;
       f2_t v[16];
-      if constexpr (KIND == KS_KERNEL_STORED) {   // K streamed from HBM: all 32 loads issued up front
-        const int64_t jb = (int64_t)c * kSrhtB + cg;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int64_t j = jb + 32 * q;
-          v[q] = j < ncols ? f2(__ldg(kr0 + j), __ldg(kr1 + j)) : 0ull;
-        }
+      if constexpr (KIND == KS_KERNEL_STORED) {   // K streamed from HBM: this chunk's values were loaded
+#pragma unroll                                 // (in flight) during the previous chunk's phases B and C
+        for (int q = 0; q < 16; ++q) v[q] = kpre[q];
 #pragma unroll
         for (int q = 0; q < 16; q += 2) {   // level h = 1 with the signs a_j = s_j folded in
           const float4 p0 = pc[32 * q], p1 = pc[32 * (q + 1)];
@@ -551,6 +558,8 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
           }
 #pragma unroll
       for (int q = 0; q < 16; ++q) *reinterpret_cast<f2_t*>(W + oA + 264 * q) = v[q];
+      if constexpr (KIND == KS_KERNEL_STORED)
+        if (c + 1 < A) load_k32(kpre, kr0, kr1, (int64_t)(c + 1) * kSrhtB + cg, ncols);
     }
     __syncthreads();
     // ---------------- phase B: pairs (b, b+16) packed for l bits 0-3, then bit 4 inside the pairs
