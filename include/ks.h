@@ -211,6 +211,45 @@ KS_API ks_status ks_apply_q(const float* Q_dev, int64_t rows, int32_t d, const f
 KS_API ks_status ks_trsolve(const float* R_dev, const float* C_dev, int32_t d, int32_t m, float tau, float* Z_dev,
                      int32_t* k_dev, ks_stream_t stream);
 
+/* ------------------------------------------------- NEXT-4: GP downstream */
+
+/* Theorem 5's stability diagnostic (reading L19: the condition number of the linear
+ * system K-hat R^{-1} with K-hat = K Omega = Y, "we are interested in the stability of the numerical
+ * system, K-hat R_k^{-1}", :359).  X = Y R^{-1} (rows x d, == Q-hat in exact arithmetic), G = X^T X;
+ *   out_dev (device float[4]) = { cond = sqrt(l_max / l_min) of G, i.e. c(X);  eps = ||G - I||_2
+ *   (Theorem 5 bounds c by sqrt((1 + eps) / (1 - eps)));  l_min;  l_max }.
+ *   Y_dev rows x d, R_dev d x d upper triangular with a nonzero diagonal (device fp32).  The extreme
+ *   eigenvalues of G - I come from min(d, 256) Lanczos steps with full reorthogonalisation (one CTA) and a
+ *   Sturm-count bisection of the tridiagonal (exact spectrum when d <= 256).
+ * ks_cond_gram writes only G (d x d) for a row block -- ranks all-reduce their G's and call
+ * ks_cond_from_gram (workspace >= 1024 * d bytes).  Errors: INVALID_ARGUMENT (null pointers, rows < 1,
+ * d < 1 or d > 1024), OOM. */
+KS_API ks_status ks_cond_diag_workspace_size(int64_t rows, int32_t d, size_t* bytes);
+KS_API ks_status ks_cond_diag(const float* Y_dev, int64_t rows, int32_t d, const float* R_dev, float* out_dev,
+                              void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+KS_API ks_status ks_cond_gram(const float* Y_dev, int64_t rows, int32_t d, const float* R_dev, float* G_dev,
+                              void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+KS_API ks_status ks_cond_from_gram(const float* G_dev, int32_t d, float* out_dev, void* ws_dev, size_t ws_bytes,
+                                   ks_stream_t stream);
+
+/* Gaussian likelihood with the low-rank covariance plus a nugget ("evaluating a Gaussian
+ * type likelihood"; SPEC.md:424-442 fixes the standard zero-mean form): Sigma = U diag(lam) U^T + sigma2 I,
+ * U rows x r with orthonormal columns (e.g. the TSQR Q), lam >= 0 (device fp32[r]), sigma2 > 0.
+ *   ks_gp_woodbury_solve: X = Sigma^{-1} B = (B - U diag(lam / (lam + sigma2)) U^T B) / sigma2
+ *                         (Woodbury), B / X rows x q device fp32 (X may not alias B).
+ *   ks_gp_loglik:         out_dev (device double[3]) = { -1/2 [n log 2 pi + log det Sigma + y^T Sigma^{-1} y],
+ *                         y^T Sigma^{-1} y, log det Sigma = sum log(lam + sigma2) + (n - r) log sigma2 }
+ *                         (determinant lemma), n = rows; y device fp32[rows].  The dot product is summed
+ *                         in fp64 in a fixed order.
+ * Workspace: ks_gp_workspace_size(rows, r, q) (q = 1 for the likelihood).  Errors: INVALID_ARGUMENT
+ * (null pointers, sizes < 1, sigma2 <= 0), OOM. */
+KS_API ks_status ks_gp_workspace_size(int64_t rows, int32_t r, int32_t q, size_t* bytes);
+KS_API ks_status ks_gp_woodbury_solve(const float* U_dev, int64_t rows, int32_t r, const float* lam_dev, float sigma2,
+                                      const float* B_dev, int32_t q, float* X_dev, void* ws_dev, size_t ws_bytes,
+                                      ks_stream_t stream);
+KS_API ks_status ks_gp_loglik(const float* U_dev, int64_t rows, int32_t r, const float* lam_dev, float sigma2,
+                              const float* y_dev, double* out_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+
 /* One-shot single-GPU path: sketch -> tsqr -> apply_qt -> trsolve -> omega_apply.
  *   A_dev n x m, X_dev n x m, Z_dev d x m, k_dev int32 (device).  Workspace
  *   size from ks_lowrank_workspace_size. */

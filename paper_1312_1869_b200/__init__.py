@@ -25,6 +25,8 @@ __all__ = [
     "ks_tsqr_merge_workspace_size", "ks_tsqr_merge", "ks_apply_qt_workspace_size", "ks_apply_qt",
     "ks_apply_q", "ks_trsolve", "ks_lowrank_workspace_size", "ks_lowrank_solve", "ks_last_error",
     "ks_version", "Sketch", "TsqrPlan", "Pipeline", "make_desc",
+    "ks_cond_diag_workspace_size", "ks_cond_diag", "ks_cond_gram", "ks_cond_from_gram", "cond_diag",
+    "ks_gp_workspace_size", "ks_gp_woodbury_solve", "ks_gp_loglik", "gp_woodbury_solve", "gp_loglik",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -59,6 +61,13 @@ _SIGS = {
     "ks_sketch_workspace_size": [C.POINTER(SketchDesc), C.POINTER(_sz)],
     "ks_sketch": [C.POINTER(SketchDesc), _P, _i64, _i64, _P, _P, _sz, _P],
     "ks_sketch_stored": [C.POINTER(SketchDesc), _P, _i64, _i64, _i64, _P, _P, _sz, _P],
+    "ks_cond_diag_workspace_size": [_i64, _i32, C.POINTER(_sz)],
+    "ks_cond_diag": [_P, _i64, _i32, _P, _P, _P, _sz, _P],
+    "ks_cond_gram": [_P, _i64, _i32, _P, _P, _P, _sz, _P],
+    "ks_cond_from_gram": [_P, _i32, _P, _P, _sz, _P],
+    "ks_gp_workspace_size": [_i64, _i32, _i32, C.POINTER(_sz)],
+    "ks_gp_woodbury_solve": [_P, _i64, _i32, _P, _f32, _P, _i32, _P, _P, _sz, _P],
+    "ks_gp_loglik": [_P, _i64, _i32, _P, _f32, _P, _P, _P, _sz, _P],
     "ks_omega_export": [C.POINTER(SketchDesc), _P, _P, _P, _P, _sz, _P],
     "ks_omega_apply": [C.POINTER(SketchDesc), _P, _i32, _i64, _i64, _P, _P, _sz, _P],
     "ks_tsqr_workspace_size": [_i64, _i32, _i32, C.POINTER(_sz)],
@@ -263,6 +272,72 @@ def ks_lowrank_solve(desc, pts, A, m, blocks, tau, X, Z, k, ws, stream=None):
                                   int(m), int(blocks), float(tau), _ptr(X, torch.float32, "X"),
                                   _ptr(Z, torch.float32, "Z"), _ptr(k, torch.int32, "k"), _ptr(ws),
                                   ws.numel() * ws.element_size(), _stream(stream)))
+
+
+# ------------------------------------------------------------ NEXT-4: Theorem 5 diagnostic, GP likelihood
+def ks_cond_diag_workspace_size(rows, d) -> int:
+    b = _sz(0)
+    _check(lib().ks_cond_diag_workspace_size(int(rows), int(d), C.byref(b)))
+    return b.value
+
+
+def ks_cond_diag(Y, R, out, ws, stream=None):
+    _check(lib().ks_cond_diag(_ptr(Y, torch.float32, "Y"), Y.shape[0], Y.shape[1], _ptr(R, torch.float32, "R"),
+                              _ptr(out, torch.float32, "out"), _ptr(ws), ws.numel() * ws.element_size(),
+                              _stream(stream)))
+
+
+def ks_cond_gram(Y, R, G, ws, stream=None):
+    _check(lib().ks_cond_gram(_ptr(Y, torch.float32, "Y"), Y.shape[0], Y.shape[1], _ptr(R, torch.float32, "R"),
+                              _ptr(G, torch.float32, "G"), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def ks_cond_from_gram(G, out, ws, stream=None):
+    _check(lib().ks_cond_from_gram(_ptr(G, torch.float32, "G"), G.shape[0], _ptr(out, torch.float32, "out"),
+                                   _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def cond_diag(Y, R, stream=None):
+    """(cond, eps, l_min, l_max) of G = (Y R^-1)^T (Y R^-1) as a device float[4] (Theorem 5 diagnostic)."""
+    ws = _ws(ks_cond_diag_workspace_size(Y.shape[0], Y.shape[1]), Y.device)
+    out = torch.empty(4, dtype=torch.float32, device=Y.device)
+    ks_cond_diag(Y, R, out, ws, stream)
+    return out
+
+
+def ks_gp_workspace_size(rows, r, q) -> int:
+    b = _sz(0)
+    _check(lib().ks_gp_workspace_size(int(rows), int(r), int(q), C.byref(b)))
+    return b.value
+
+
+def ks_gp_woodbury_solve(U, lam, sigma2, B, X, ws, stream=None):
+    _check(lib().ks_gp_woodbury_solve(_ptr(U, torch.float32, "U"), U.shape[0], U.shape[1],
+                                      _ptr(lam, torch.float32, "lam"), float(sigma2), _ptr(B, torch.float32, "B"),
+                                      B.shape[1], _ptr(X, torch.float32, "X"), _ptr(ws),
+                                      ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def ks_gp_loglik(U, lam, sigma2, y, out, ws, stream=None):
+    _check(lib().ks_gp_loglik(_ptr(U, torch.float32, "U"), U.shape[0], U.shape[1], _ptr(lam, torch.float32, "lam"),
+                              float(sigma2), _ptr(y, torch.float32, "y"), _ptr(out, torch.float64, "out"), _ptr(ws),
+                              ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def gp_woodbury_solve(U, lam, sigma2, B, stream=None):
+    B2 = B if B.dim() == 2 else B.reshape(-1, 1)
+    ws = _ws(ks_gp_workspace_size(U.shape[0], U.shape[1], B2.shape[1]), U.device)
+    X = torch.empty_like(B2)
+    ks_gp_woodbury_solve(U, lam, sigma2, B2, X, ws, stream)
+    return X.reshape(B.shape)
+
+
+def gp_loglik(U, lam, sigma2, y, stream=None):
+    """Device double[3]: (log-likelihood, y^T Sigma^-1 y, log det Sigma)."""
+    ws = _ws(ks_gp_workspace_size(U.shape[0], U.shape[1], 1), U.device)
+    out = torch.empty(3, dtype=torch.float64, device=U.device)
+    ks_gp_loglik(U, lam, sigma2, y, out, ws, stream)
+    return out
 
 
 # ------------------------------------------------------------ workspace bundles

@@ -132,6 +132,78 @@ extern "C" ks_status ks_apply_q(const float* Q, int64_t rows, int32_t d, const f
   KS_GUARD_END
 }
 
+// ------------------------------------------------------------------ NEXT-4
+extern "C" ks_status ks_cond_diag_workspace_size(int64_t rows, int32_t d, size_t* bytes) {
+  if (!bytes || rows < 1 || d < 1 || d > 1024) return fail(KS_ERR_INVALID_ARGUMENT, "need rows >= 1, 1 <= d <= 1024");
+  return cond_diag_ws(rows, d, bytes);
+}
+
+static ks_status cond_check(const float* Y, int64_t rows, int32_t d, const float* R, const void* out, void* ws,
+                            size_t ws_bytes) {
+  size_t need = 0;
+  KS_TRY(ks_cond_diag_workspace_size(rows, d, &need));
+  if (!Y || !R || !out || !ws) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if (ws_bytes < need) return fail(KS_ERR_OOM, "cond workspace too small: need " + std::to_string(need));
+  return KS_OK;
+}
+
+extern "C" ks_status ks_cond_diag(const float* Y, int64_t rows, int32_t d, const float* R, float* out, void* ws,
+                                  size_t ws_bytes, ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  KS_TRY(cond_check(Y, rows, d, R, out, ws, ws_bytes));
+  return cond_diag_run(Y, rows, d, R, out, static_cast<char*>(ws), S(stream));
+  KS_GUARD_END
+}
+
+extern "C" ks_status ks_cond_gram(const float* Y, int64_t rows, int32_t d, const float* R, float* G, void* ws,
+                                  size_t ws_bytes, ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  KS_TRY(cond_check(Y, rows, d, R, G, ws, ws_bytes));
+  return cond_gram_run(Y, rows, d, R, G, static_cast<char*>(ws), S(stream));
+  KS_GUARD_END
+}
+
+extern "C" ks_status ks_cond_from_gram(const float* G, int32_t d, float* out, void* ws, size_t ws_bytes,
+                                       ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  if (!G || !out || !ws || d < 1 || d > 1024) return fail(KS_ERR_INVALID_ARGUMENT, "invalid argument");
+  if (ws_bytes < cond_from_gram_ws(d))
+    return fail(KS_ERR_OOM, "cond workspace too small: need " + std::to_string(cond_from_gram_ws(d)));
+  return cond_from_gram_run(G, d, out, static_cast<float*>(ws), S(stream));
+  KS_GUARD_END
+}
+
+extern "C" ks_status ks_gp_workspace_size(int64_t rows, int32_t r, int32_t q, size_t* bytes) {
+  if (!bytes || rows < 1 || r < 1 || q < 1) return fail(KS_ERR_INVALID_ARGUMENT, "need rows, r, q >= 1");
+  return gp_ws(rows, r, q, bytes);
+}
+
+extern "C" ks_status ks_gp_woodbury_solve(const float* U, int64_t rows, int32_t r, const float* lam, float sigma2,
+                                          const float* B, int32_t q, float* X, void* ws, size_t ws_bytes,
+                                          ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  size_t need = 0;
+  KS_TRY(ks_gp_workspace_size(rows, r, q, &need));
+  if (!U || !lam || !B || !X || !ws) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if (!(sigma2 > 0.f) || !std::isfinite(sigma2)) return fail(KS_ERR_INVALID_ARGUMENT, "sigma2 must be > 0");
+  if (X == B) return fail(KS_ERR_INVALID_ARGUMENT, "X may not alias B");
+  if (ws_bytes < need) return fail(KS_ERR_OOM, "gp workspace too small: need " + std::to_string(need));
+  return gp_woodbury_run(U, rows, r, lam, sigma2, B, q, X, static_cast<char*>(ws), S(stream));
+  KS_GUARD_END
+}
+
+extern "C" ks_status ks_gp_loglik(const float* U, int64_t rows, int32_t r, const float* lam, float sigma2,
+                                  const float* y, double* out, void* ws, size_t ws_bytes, ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  size_t need = 0;
+  KS_TRY(ks_gp_workspace_size(rows, r, 1, &need));
+  if (!U || !lam || !y || !out || !ws) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if (!(sigma2 > 0.f) || !std::isfinite(sigma2)) return fail(KS_ERR_INVALID_ARGUMENT, "sigma2 must be > 0");
+  if (ws_bytes < need) return fail(KS_ERR_OOM, "gp workspace too small: need " + std::to_string(need));
+  return gp_loglik_run(U, rows, r, lam, sigma2, y, out, static_cast<char*>(ws), S(stream));
+  KS_GUARD_END
+}
+
 extern "C" ks_status ks_trsolve(const float* R, const float* C, int32_t d, int32_t m, float tau, float* Z,
                                 int32_t* k_dev, ks_stream_t stream) {
   KS_GUARD_BEGIN

@@ -78,10 +78,23 @@ ks_status gauss_sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, in
 void tsqr_set_graphs(ks_tsqr_handle h, bool on);
 
 // ---------------------------------------------------------------- solve side
+// NEXT-4 (ks_gp.cu)
+ks_status cond_diag_ws(int64_t rows, int d, size_t* bytes);
+ks_status cond_gram_run(const float* Y, int64_t rows, int d, const float* R, float* G, char* ws, cudaStream_t st);
+ks_status cond_from_gram_run(const float* G, int d, float* out, float* V, cudaStream_t st);
+size_t cond_from_gram_ws(int d);
+ks_status cond_diag_run(const float* Y, int64_t rows, int d, const float* R, float* out, char* ws, cudaStream_t st);
+ks_status gp_ws(int64_t rows, int r, int q, size_t* bytes);
+ks_status gp_woodbury_run(const float* U, int64_t rows, int r, const float* lam, float s2, const float* B, int q,
+                          float* X, char* ws, cudaStream_t st);
+ks_status gp_loglik_run(const float* U, int64_t rows, int r, const float* lam, float s2, const float* y, double* out,
+                        char* ws, cudaStream_t st);
 ks_status apply_qt_ws(int64_t rows, int d, int m, size_t* bytes);
 ks_status apply_qt_run(const float* Q, int64_t rows, int d, const float* X, int m, float* C, void* ws,
                        cudaStream_t st);
-ks_status apply_q_run(const float* Q, int64_t rows, int d, const float* C, int m, float* X, cudaStream_t st);
+// X = Q C, or X = alpha B + beta Q C when B != nullptr (any m).
+ks_status apply_q_run(const float* Q, int64_t rows, int d, const float* C, int m, float* X, cudaStream_t st,
+                      const float* B = nullptr, float alpha = 0.f, float beta = 1.f);
 ks_status trsolve_run(const float* R, const float* C, int d, int m, float tau, float* Z, int32_t* k,
                       cudaStream_t st);
 

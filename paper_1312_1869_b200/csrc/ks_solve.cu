@@ -6,19 +6,22 @@
 #include "ks_common.cuh"
 #include "ks_internal.h"
 
+#include <algorithm>
+
 namespace ks {
 
 constexpr int kQtRows = 1024;  // rows per partial chunk
 
 // Partial C_chunk[dt*64 .. +64, 0 .. m) = Q[rows of chunk]^T X[rows of chunk].
 __global__ void __launch_bounds__(256) k_qtx_partial(const float* __restrict__ Q, int64_t rows, int d,
-                                                     const float* __restrict__ X, int m, float* __restrict__ part) {
+                                                     const float* __restrict__ X, int m, float* __restrict__ part,
+                                                     int64_t chunk_rows) {
   __shared__ float Qs[32][64 + 4];
   __shared__ float Xs[32][64 + 4];
-  const int chunk = blockIdx.x, dt = blockIdx.y;
+  const int chunk = blockIdx.x, dt = blockIdx.y, mt = blockIdx.z;   // 64 x 64 tile (dt, mt) of C
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const int64_t r0 = (int64_t)chunk * kQtRows;
-  const int64_t r1 = min(rows, r0 + kQtRows);
+  const int64_t r0 = (int64_t)chunk * chunk_rows;
+  const int64_t r1 = min(rows, r0 + chunk_rows);
   float acc[4][4] = {};
   for (int64_t rs = r0; rs < r1; rs += 32) {
     for (int p = tid; p < 32 * 64; p += 256) {
@@ -26,7 +29,7 @@ __global__ void __launch_bounds__(256) k_qtx_partial(const float* __restrict__ Q
       const int64_t r = rs + rr;
       const int dc = dt * 64 + cc;
       Qs[rr][cc] = (r < r1 && dc < d) ? Q[r * d + dc] : 0.f;
-      Xs[rr][cc] = (r < r1 && cc < m) ? X[r * m + cc] : 0.f;
+      Xs[rr][cc] = (r < r1 && mt * 64 + cc < m) ? X[r * m + mt * 64 + cc] : 0.f;
     }
     __syncthreads();
 #pragma unroll 8
@@ -46,7 +49,7 @@ __global__ void __launch_bounds__(256) k_qtx_partial(const float* __restrict__ Q
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int dr = dt * 64 + 4 * ty + a, mc = 4 * tx + c;
+      const int dr = dt * 64 + 4 * ty + a, mc = mt * 64 + 4 * tx + c;
       if (dr < d && mc < m) P[dr * m + mc] = acc[a][c];
     }
 }
@@ -60,12 +63,16 @@ __global__ void k_qtx_reduce(const float* __restrict__ part, int nchunks, int dm
 }
 
 // X (rows x m) = Q (rows x d) C (d x m)
+// (general form: X = alpha B + beta Q C when B != nullptr; 64-column tiles of C / X by blockIdx.y)
 __global__ void __launch_bounds__(256) k_qc(const float* __restrict__ Q, int64_t rows, int d,
-                                            const float* __restrict__ C, int m, float* __restrict__ X) {
+                                            const float* __restrict__ C, int m, float* __restrict__ X,
+                                            const float* __restrict__ B = nullptr, float alpha = 0.f,
+                                            float beta = 1.f) {
   __shared__ float Qs[32][33];
   __shared__ float Cs[32][64 + 4];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int m0 = 64 * blockIdx.y;
   float acc[2][4] = {};
   for (int k0 = 0; k0 < d; k0 += 32) {
     for (int p = tid; p < 32 * 32; p += 256) {
@@ -74,7 +81,7 @@ __global__ void __launch_bounds__(256) k_qc(const float* __restrict__ Q, int64_t
     }
     for (int p = tid; p < 32 * 64; p += 256) {
       const int kk = p >> 6, cc = p & 63;
-      Cs[kk][cc] = (k0 + kk < d && cc < m) ? C[(k0 + kk) * m + cc] : 0.f;
+      Cs[kk][cc] = (k0 + kk < d && m0 + cc < m) ? C[(k0 + kk) * m + m0 + cc] : 0.f;
     }
     __syncthreads();
 #pragma unroll 8
@@ -91,8 +98,8 @@ __global__ void __launch_bounds__(256) k_qc(const float* __restrict__ Q, int64_t
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int64_t r = r0 + 2 * ty + a;
-      const int mc = 4 * tx + c;
-      if (r < rows && mc < m) X[r * m + mc] = acc[a][c];
+      const int mc = m0 + 4 * tx + c;
+      if (r < rows && mc < m) X[r * m + mc] = B ? fmaf(alpha, B[r * m + mc], beta * acc[a][c]) : acc[a][c];
     }
 }
 
@@ -202,25 +209,34 @@ __global__ void __launch_bounds__(256) k_trsolve(const float* __restrict__ R, co
   }
 }
 
+// Rows per partial chunk: kQtRows, doubled while the chunks' (d x m) partials would exceed 64 MiB.
+static int64_t qt_chunk_rows(int64_t rows, int d, int m) {
+  int64_t c = kQtRows;
+  while (((rows + c - 1) / c) * (int64_t)d * m * 4 > (int64_t(64) << 20)) c *= 2;
+  return c;
+}
+
 ks_status apply_qt_ws(int64_t rows, int d, int m, size_t* bytes) {
-  const int64_t nchunks = (rows + kQtRows - 1) / kQtRows;
+  const int64_t cr = qt_chunk_rows(rows, d, m), nchunks = (rows + cr - 1) / cr;
   *bytes = sizeof(float) * (size_t)nchunks * d * m;
   return KS_OK;
 }
 
 ks_status apply_qt_run(const float* Q, int64_t rows, int d, const float* X, int m, float* C, void* ws, cudaStream_t st) {
-  const int64_t nchunks = (rows + kQtRows - 1) / kQtRows;
+  const int64_t cr = qt_chunk_rows(rows, d, m), nchunks = (rows + cr - 1) / cr;
   float* part = static_cast<float*>(ws);
-  dim3 grid((unsigned)nchunks, (unsigned)((d + 63) / 64));
-  k_qtx_partial<<<grid, 256, 0, st>>>(Q, rows, d, X, m, part);
+  dim3 grid((unsigned)nchunks, (unsigned)((d + 63) / 64), (unsigned)((m + 63) / 64));
+  k_qtx_partial<<<grid, 256, 0, st>>>(Q, rows, d, X, m, part, cr);
   KS_LAUNCH_CHECK();
   k_qtx_reduce<<<(d * m + 255) / 256, 256, 0, st>>>(part, (int)nchunks, d * m, C);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }
 
-ks_status apply_q_run(const float* Q, int64_t rows, int d, const float* C, int m, float* X, cudaStream_t st) {
-  k_qc<<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(Q, rows, d, C, m, X);
+ks_status apply_q_run(const float* Q, int64_t rows, int d, const float* C, int m, float* X, cudaStream_t st,
+                      const float* B, float alpha, float beta) {
+  k_qc<<<dim3((unsigned)((rows + 31) / 32), (unsigned)((m + 63) / 64)), 256, 0, st>>>(Q, rows, d, C, m, X, B, alpha,
+                                                                                     beta);
   KS_LAUNCH_CHECK();
   return KS_OK;
 }

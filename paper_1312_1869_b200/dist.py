@@ -112,3 +112,18 @@ def lowrank_solve_sharded(ops, pts, A_local, group=None):
     Z, k = ops.trsolve(R, Cm)
     X = ops.omega_apply(Z)
     return X, Z, k, R
+
+
+def cond_diag_sharded(Y_local, R, group=None):
+    """Theorem 5 diagnostic over row-sharded Y (NEXT-4): per-rank Gram of Y R^-1 (ks_cond_gram), summed
+    with one all-reduce, then the extreme eigenvalues (ks_cond_from_gram).  Returns the device float[4]
+    (cond, eps, l_min, l_max)."""
+    from . import _ws, ks_cond_diag_workspace_size, ks_cond_from_gram, ks_cond_gram
+    rows, d = Y_local.shape
+    G = torch.empty((d, d), dtype=torch.float32, device=Y_local.device)
+    ks_cond_gram(Y_local, R, G, _ws(ks_cond_diag_workspace_size(rows, d), Y_local.device))
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
+    out = torch.empty(4, dtype=torch.float32, device=Y_local.device)
+    ks_cond_from_gram(G, out, _ws(1024 * d, Y_local.device))
+    return out

@@ -1,0 +1,116 @@
+"""NEXT-4 on the GPU: Theorem 5's diagnostic (ks_cond_diag) and the GP Woodbury solve / log-likelihood
+(ks_gp_woodbury_solve, ks_gp_loglik) against oracle/gp.py on the same fp32 inputs."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import gp
+from _problems import desc_of, problem, relF
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a, cuda):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a, np.float32), device=cuda)
+
+
+def _orth(n, r, seed):
+    Q, _ = np.linalg.qr(np.random.default_rng(seed).standard_normal((n, r)))
+    return Q.astype(np.float32)
+
+
+@pytest.mark.parametrize("n,d", [(4000, 64), (1000, 200), (3333, 512)])
+def test_cond_diag_known_singular_values(ks, cuda, n, d):
+    Q = _orth(n, d, 1).astype(np.float64)
+    s = np.linspace(0.6, 1.3, d)
+    V = _orth(d, d, 2).astype(np.float64)
+    Y = ((Q * s) @ V.T).astype(np.float32)
+    R = np.triu(np.eye(d) + 0.1 * np.random.default_rng(3).standard_normal((d, d))).astype(np.float32)
+    R[np.diag_indices(d)] = np.abs(R[np.diag_indices(d)]) + 0.5
+    out = ks.cond_diag(_t(Y, cuda), _t(R, cuda)).cpu().numpy()
+    c, eps, lo, hi = gp.cond_diag(Y, R)
+    tol = 1e-3 if d <= 256 else 1e-2     # d <= 256: the whole Lanczos spectrum; d = 512: 256 steps
+    assert abs(out[0] - c) <= tol * c
+    assert abs(out[2] - lo) <= 2 * tol * lo and abs(out[3] - hi) <= tol * hi
+    assert abs(out[1] - eps) <= tol * max(eps, 1e-3)
+
+
+@pytest.mark.parametrize("name,over,blocks", [("c2", dict(n=6000, d=64), 4), ("c3", dict(n=4096, d=128), 2)])
+def test_cond_diag_of_the_pipeline_is_near_one(ks, cuda, name, over, blocks):
+    """Theorem 5: c(K-hat R^{-1}) <= sqrt((1 + eps) / (1 - eps)); with the sketch and TSQR of the configs
+    the GPU's diagnostic is ~1 and agrees with the oracle's fp64 evaluation on the same fp32 Y, R."""
+    cfg, pts, A, prob = problem(name, **over)
+    sk = ks.Sketch(desc_of(cfg), cuda)
+    Y = sk(_t(pts, cuda))
+    plan = ks.TsqrPlan(cfg["n"], cfg["d"], blocks, cuda)
+    Q, R = plan.factor(Y)
+    out = ks.cond_diag(Y, R).cpu().numpy()
+    c, eps, lo, hi = gp.cond_diag(Y.cpu().numpy(), R.cpu().numpy())
+    assert c <= np.sqrt(2.0) and out[0] <= np.sqrt(2.0)              # Thm 5 with eps = 1/3
+    assert abs(out[0] - c) <= 1e-3
+    assert out[1] <= 1.0 / 3.0
+
+
+def test_gp_woodbury_and_loglik_match_oracle(ks, cuda):
+    n, r, q, s2 = 3000, 32, 5, float(np.float32(0.1))   # (sigma2 as the fp32 the C-ABI receives)
+    U = _orth(n, r, 4)
+    lam = (10.0 * np.exp(-np.arange(r) / 6.0)).astype(np.float32)
+    rng = np.random.default_rng(5)
+    B = rng.standard_normal((n, q)).astype(np.float32)
+    y = rng.standard_normal(n).astype(np.float32)
+    X = ks.gp_woodbury_solve(_t(U, cuda), _t(lam, cuda), s2, _t(B, cuda)).cpu().numpy()
+    Xr = gp.woodbury_solve(U, lam, s2, B)
+    assert relF(X, Xr) <= 1e-5
+    out = ks.gp_loglik(_t(U, cuda), _t(lam, cuda), s2, _t(y, cuda)).cpu().numpy()
+    ll, quad, logdet = gp.log_likelihood(U, lam, s2, y)
+    assert abs(out[1] - quad) <= 1e-5 * abs(quad)
+    assert abs(out[2] - logdet) <= 1e-9 * abs(logdet)
+    assert abs(out[0] - ll) <= 1e-5 * abs(ll)
+
+
+def test_gp_loglik_with_the_pipeline_factor(ks, cuda):
+    """U = the TSQR Q of a sketch (orthonormal to fp32 accuracy), lam = 0: the likelihood reduces to the
+    white-noise density N(0, s2 I) -- a closed form."""
+    cfg, pts, A, prob = problem("c1", n=2048, d=64)
+    Y = ks.Sketch(desc_of(cfg), cuda)(_t(pts, cuda))
+    Q, R = ks.TsqrPlan(2048, 64, 2, cuda).factor(Y)
+    y = np.random.default_rng(6).standard_normal(2048).astype(np.float32)
+    s2 = float(np.float32(0.4))
+    out = ks.gp_loglik(Q, _t(np.zeros(64, np.float32), cuda), s2, _t(y, cuda)).cpu().numpy()
+    yy = float(np.dot(y.astype(np.float64), y.astype(np.float64)))
+    ref = -0.5 * (2048 * np.log(2 * np.pi) + 2048 * np.log(s2) + yy / s2)
+    assert abs(out[0] - ref) <= 1e-6 * abs(ref)
+
+
+def test_gp_argument_errors(ks, cuda):
+    import torch
+    U = _t(_orth(100, 4, 7), cuda)
+    lam = _t(np.ones(4), cuda)
+    B = _t(np.ones((100, 1)), cuda)
+    with pytest.raises(ks.KsError):
+        ks.gp_woodbury_solve(U, lam, 0.0, B)          # sigma2 must be > 0
+    ws = torch.empty(16, dtype=torch.uint8, device=cuda)
+    with pytest.raises(ks.KsError):
+        ks.ks_gp_woodbury_solve(U, lam, 1.0, B, torch.empty_like(B), ws)   # workspace too small
+
+
+def test_cond_split_api_matches_one_call(ks, cuda):
+    """ks_cond_gram on row blocks, summed (what ranks all-reduce), then ks_cond_from_gram == ks_cond_diag."""
+    import torch
+    n, d = 5000, 96
+    Y = _t(np.random.default_rng(11).standard_normal((n, d)), cuda)
+    Q, R = ks.TsqrPlan(n, d, 2, cuda).factor(Y)
+    one = ks.cond_diag(Y, R).cpu().numpy()
+    G = torch.zeros((d, d), dtype=torch.float32, device=cuda)
+    for rb, re in ((0, 2100), (2100, n)):
+        Yb = Y[rb:re].contiguous()
+        ws = torch.empty(ks.ks_cond_diag_workspace_size(re - rb, d), dtype=torch.uint8, device=cuda)
+        Gb = torch.empty((d, d), dtype=torch.float32, device=cuda)
+        ks.ks_cond_gram(Yb, R, Gb, ws)
+        G += Gb
+    out = torch.empty(4, dtype=torch.float32, device=cuda)
+    ks.ks_cond_from_gram(G, out, torch.empty(1024 * d, dtype=torch.uint8, device=cuda))
+    out = out.cpu().numpy()
+    c, eps, lo, hi = gp.cond_diag(Y.cpu().numpy(), R.cpu().numpy())
+    assert abs(out[0] - one[0]) <= 1e-5 and abs(out[0] - c) <= 1e-4
