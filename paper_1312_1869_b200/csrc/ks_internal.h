@@ -30,6 +30,16 @@ void add_launches(uint64_t n);   // kernels of a replayed CUDA graph
     KS_CUDA_TRY(cudaGetLastError());     \
   } while (0)
 
+// Streaming multiprocessors of the current device (persistent-grid sizing), queried once.
+inline int num_sms() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
 #define KS_TRY(expr)                     \
   do {                                   \
     ks_status s__ = (expr);              \
