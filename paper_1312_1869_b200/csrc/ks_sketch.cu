@@ -697,12 +697,20 @@ __global__ void __launch_bounds__(256) k_omega_apply_srht(const float* __restric
     }
     __syncthreads();
   }
+  // X rows of this chunk: a warp per row, lanes along the columns (coalesced row writes)
+  __shared__ float srow[kSrhtB];
   for (int l = tid; l < kSrhtB; l += 256) {
     const int64_t j = (int64_t)c * kSrhtB + l;
+    srow[l] = (j < n) ? rademacher(seed, j) * scale : 0.f;
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int l = warp; l < kSrhtB; l += 8) {
+    const int64_t j = (int64_t)c * kSrhtB + l;
     if (j < row_begin || j >= row_end || j >= n) continue;
-    const float s = rademacher(seed, j) * scale;
+    const float s = srow[l];
     float* xr = X + (j - row_begin) * (int64_t)m;
-    for (int col = 0; col < m; ++col) xr[col] = s * u[l * ld + col];
+    for (int col = lane; col < m; col += 32) xr[col] = s * u[l * ld + col];
   }
 }
 

@@ -54,6 +54,91 @@ __global__ void __launch_bounds__(256) k_qtx_partial(const float* __restrict__ Q
     }
 }
 
+// Fast path (d % 4 == 0, m % 4 == 0): a CTA owns a 256 x MT tile of C over a chunk of rows.  32-row slabs
+// of Q (32 x 256) and X (32 x MT) are double buffered in shared memory by cp.async (zero-filled outside
+// the matrix); thread (tx, ty) accumulates an 8 x (MT/8) micro-tile with packed f32x2 FMAs, the
+// broadcast operands read as LDS.128 (Q: 4 distinct 32-B rows per warp, X: 8 distinct) -- 2 FMA per byte
+// of shared memory read.
+KS_DEVINL void qt_cp16(void* sdst, const void* gsrc, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(ok ? 16 : 0)
+               : "memory");
+}
+template <int MT>
+__global__ void __launch_bounds__(256, 2) k_qtx_fast(const float* __restrict__ Q, int64_t rows, int d,
+                                                    const float* __restrict__ X, int m, float* __restrict__ part,
+                                                    int64_t chunk_rows) {
+  constexpr int MU = MT / 8;               // m columns per thread
+  extern __shared__ __align__(16) float qsm[];
+  float* Qs = qsm;                         // [2][32][256]
+  float* Xs = qsm + 2 * 32 * 256;          // [2][32][MT]
+  const int chunk = blockIdx.x, d0 = 256 * blockIdx.y, m0 = MT * blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = lane & 7, ty = 4 * warp + (lane >> 3);
+  const int64_t r0 = (int64_t)chunk * chunk_rows;
+  const int64_t r1 = min(rows, r0 + chunk_rows);
+  auto issue = [&](int64_t rs, int b) {
+    float* qb = Qs + b * (32 * 256);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {   // 32 rows x 64 chunks of 16 B
+      const int p = tid + 256 * i, rr = p >> 6, c4 = 4 * (p & 63);
+      const bool ok = rs + rr < r1 && d0 + c4 < d;
+      qt_cp16(qb + rr * 256 + c4, ok ? Q + (rs + rr) * d + d0 + c4 : Q, ok);
+    }
+    float* xb = Xs + b * (32 * MT);
+    for (int p = tid; p < 32 * (MT / 4); p += 256) {
+      const int rr = p / (MT / 4), c4 = 4 * (p % (MT / 4));
+      const bool ok = rs + rr < r1 && m0 + c4 < m;
+      qt_cp16(xb + rr * MT + c4, ok ? X + (rs + rr) * m + m0 + c4 : X, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  f2_t acc[8][MU / 2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int c = 0; c < MU / 2; ++c) acc[a][c] = 0ull;
+  if (r0 < r1) issue(r0, 0);
+  int b = 0;
+  for (int64_t rs = r0; rs < r1; rs += 32, b ^= 1) {
+    if (rs + 32 < r1) issue(rs + 32, b ^ 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const float* qb = Qs + b * (32 * 256) + 8 * ty;
+    const float* xb = Xs + b * (32 * MT) + MU * tx;
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      const float4 qa = *reinterpret_cast<const float4*>(qb + rr * 256);
+      const float4 qc = *reinterpret_cast<const float4*>(qb + rr * 256 + 4);
+      const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qc.x, qc.y, qc.z, qc.w};
+      f2_t xv[MU / 2];
+#pragma unroll
+      for (int c4 = 0; c4 < MU / 4; ++c4) {
+        const float4 x = *reinterpret_cast<const float4*>(xb + rr * MT + 4 * c4);
+        xv[2 * c4] = f2(x.x, x.y);
+        xv[2 * c4 + 1] = f2(x.z, x.w);
+      }
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int c = 0; c < MU / 2; ++c) acc[a][c] = f2fma(f2s(qv[a]), xv[c], acc[a][c]);
+    }
+    __syncthreads();   // buffer b is refilled by the next-but-one issue
+  }
+  float* P = part + (int64_t)chunk * d * m;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int dr = d0 + 8 * ty + a;
+    if (dr >= d) continue;
+#pragma unroll
+    for (int c = 0; c < MU / 2; ++c) {
+      const int mc = m0 + MU * tx + 2 * c;
+      if (mc < m) P[(int64_t)dr * m + mc] = f2lo(acc[a][c]);
+      if (mc + 1 < m) P[(int64_t)dr * m + mc + 1] = f2hi(acc[a][c]);
+    }
+  }
+}
+
 __global__ void k_qtx_reduce(const float* __restrict__ part, int nchunks, int dm, float* __restrict__ C) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= dm) return;
@@ -225,6 +310,29 @@ ks_status apply_qt_ws(int64_t rows, int d, int m, size_t* bytes) {
 ks_status apply_qt_run(const float* Q, int64_t rows, int d, const float* X, int m, float* C, void* ws, cudaStream_t st) {
   const int64_t cr = qt_chunk_rows(rows, d, m), nchunks = (rows + cr - 1) / cr;
   float* part = static_cast<float*>(ws);
+  const bool fast = (d & 3) == 0 && (m & 3) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  if (fast) {
+    // ~2 CTAs per SM: chunks of >= cr rows (fewer partials than the workspace holds), multiples of 32
+    const int mt = m <= 32 ? 32 : 64;
+    const int64_t tiles = (int64_t)((d + 255) / 256) * ((m + mt - 1) / mt);
+    int64_t fc = (rows * tiles + 2 * num_sms() - 1) / (2 * num_sms());
+    fc = std::max<int64_t>(cr, (fc + 31) / 32 * 32);
+    const int64_t nc = (rows + fc - 1) / fc;
+    dim3 grid((unsigned)nc, (unsigned)((d + 255) / 256), (unsigned)((m + mt - 1) / mt));
+    const int smem = (int)sizeof(float) * 2 * 32 * (256 + mt);
+    if (mt == 32) {
+      KS_CUDA_TRY(cudaFuncSetAttribute(k_qtx_fast<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_qtx_fast<32><<<grid, 256, smem, st>>>(Q, rows, d, X, m, part, fc);
+    } else {
+      KS_CUDA_TRY(cudaFuncSetAttribute(k_qtx_fast<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_qtx_fast<64><<<grid, 256, smem, st>>>(Q, rows, d, X, m, part, fc);
+    }
+    KS_LAUNCH_CHECK();
+    k_qtx_reduce<<<(d * m + 255) / 256, 256, 0, st>>>(part, (int)nc, d * m, C);
+    KS_LAUNCH_CHECK();
+    return KS_OK;
+  }
   dim3 grid((unsigned)nchunks, (unsigned)((d + 63) / 64), (unsigned)((m + 63) / 64));
   k_qtx_partial<<<grid, 256, 0, st>>>(Q, rows, d, X, m, part, cr);
   KS_LAUNCH_CHECK();
