@@ -665,52 +665,75 @@ ks_status sketch_run(const ks_sketch_desc& D, const SketchLayout& L, int64_t rb,
 // ============================================================ Omega-apply
 // SRHT: X[j, col] = s_j / sqrt(N) * (H_N scatter_S(Z[:, col]))[j]  (Omega Z with Omega^T = (1/sqrt N) H[S,:] D_s).
 // Per chunk c (rows j = cB + l):  u[m] = sum_{t: m_t = m} (-1)^popc(c & a_t) Z[t, col];  X = s o FWHT_B(u).
+// CTA = (chunk c, 32-column tile of Z): the bucket CSR and the chunk signs of the d outputs are staged in
+// shared memory, u = scatter(Z) (a warp per bucket row, lanes along the columns), FWHT_512 as three radix-8
+// passes in shared memory, then coalesced row writes of s_j u / sqrt N.
+constexpr int kOaCols = 32;
 __global__ void __launch_bounds__(256) k_omega_apply_srht(const float* __restrict__ Z, int m, int d,
                                                           const uint32_t* __restrict__ tab,
                                                           const int32_t* __restrict__ bofs,
                                                           const int32_t* __restrict__ bidx, uint64_t seed,
                                                           int64_t n, int64_t row_begin, int64_t row_end,
                                                           int c_first, float scale, float* __restrict__ X) {
-  extern __shared__ float u[];  // [kSrhtB][m + 1]
-  const int ld = m + 1;
+  constexpr int ld = kOaCols + 1;
+  extern __shared__ float u[];          // [kSrhtB][ld]
+  __shared__ int s_bofs[kSrhtB + 1];
+  __shared__ int s_bidx[512];
+  __shared__ float s_sgn[512];          // (-1)^popc(c & a_t), by output t
+  __shared__ float srow[kSrhtB];        // s_j / sqrt N of this chunk's rows
   const int c = c_first + blockIdx.x;
-  const int tid = threadIdx.x;
-  for (int p = tid; p < kSrhtB * m; p += 256) {
-    const int l = p / m, col = p - l * m;
-    float acc = 0.f;
-    for (int q = bofs[l]; q < bofs[l + 1]; ++q) {
-      const int tt = bidx[q];
-      const uint32_t a = tab[tt] >> 16;
-      const float v = Z[tt * m + col];
-      acc += (__popc((uint32_t)c & a) & 1) ? -v : v;
-    }
-    u[l * ld + col] = acc;
+  const int col0 = kOaCols * blockIdx.y, ncol = min(kOaCols, m - col0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int l = tid; l <= kSrhtB; l += 256) s_bofs[l] = bofs[l];
+  for (int t = tid; t < d; t += 256) {
+    s_bidx[t] = bidx[t];
+    s_sgn[t] = (__popc((uint32_t)c & (tab[t] >> 16)) & 1) ? -1.f : 1.f;
   }
-  __syncthreads();
-  for (int h = 1; h < kSrhtB; h <<= 1) {
-    for (int p = tid; p < (kSrhtB / 2) * m; p += 256) {
-      const int b = p / m, col = p - b * m;
-      const int l = ((b / h) * 2 * h) + (b % h);
-      const float x = u[l * ld + col], y = u[(l + h) * ld + col];
-      u[l * ld + col] = x + y;
-      u[(l + h) * ld + col] = x - y;
-    }
-    __syncthreads();
-  }
-  // X rows of this chunk: a warp per row, lanes along the columns (coalesced row writes)
-  __shared__ float srow[kSrhtB];
   for (int l = tid; l < kSrhtB; l += 256) {
     const int64_t j = (int64_t)c * kSrhtB + l;
     srow[l] = (j < n) ? rademacher(seed, j) * scale : 0.f;
   }
   __syncthreads();
-  const int lane = tid & 31, warp = tid >> 5;
+  // ---- scatter: u[l][col] = sum over the outputs t of bucket l of sgn_t Z[t][col]
+  for (int l = warp; l < kSrhtB; l += 8) {
+    float acc = 0.f;
+    if (lane < ncol) {
+      for (int q = s_bofs[l]; q < s_bofs[l + 1]; ++q) {
+        const int tt = s_bidx[q];
+        acc = fmaf(s_sgn[tt], Z[(int64_t)tt * m + col0 + lane], acc);
+      }
+    }
+    u[l * ld + lane] = acc;
+  }
+  __syncthreads();
+  // ---- FWHT_512: three radix-8 passes (strides 1, 8, 64); item = (group g of 8, column)
+#pragma unroll 1
+  for (int h = 1; h < kSrhtB; h *= 8) {
+    for (int it = tid; it < 64 * kOaCols; it += 256) {
+      const int g = it >> 5, col = it & 31;
+      const int base = (g / h) * 8 * h + (g % h);
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = u[(base + k * h) * ld + col];
+#pragma unroll
+      for (int hh = 1; hh < 8; hh <<= 1)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (!(k & hh)) {
+            const float x = v[k], y = v[k + hh];
+            v[k] = x + y;
+            v[k + hh] = x - y;
+          }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) u[(base + k * h) * ld + col] = v[k];
+    }
+    __syncthreads();
+  }
+  // ---- X rows of this chunk: a warp per row, lanes along the columns (coalesced row writes)
   for (int l = warp; l < kSrhtB; l += 8) {
     const int64_t j = (int64_t)c * kSrhtB + l;
-    if (j < row_begin || j >= row_end || j >= n) continue;
-    const float s = srow[l];
-    float* xr = X + (j - row_begin) * (int64_t)m;
-    for (int col = lane; col < m; col += 32) xr[col] = s * u[l * ld + col];
+    if (j < row_begin || j >= row_end || j >= n || lane >= ncol) continue;
+    X[(j - row_begin) * (int64_t)m + col0 + lane] = srow[l] * u[l * ld + lane];
   }
 }
 
@@ -745,9 +768,9 @@ ks_status omega_apply_run(const ks_sketch_desc& D, const SketchLayout& L, const 
   if (re <= rb) return KS_OK;
   if (D.omega == KS_OMEGA_SRHT) {
     const int c0 = (int)(rb / kSrhtB), c1 = (int)((re - 1) / kSrhtB);
-    const int smem = kSrhtB * (m + 1) * (int)sizeof(float);
+    const int smem = kSrhtB * (kOaCols + 1) * (int)sizeof(float);
     KS_CUDA_TRY(cudaFuncSetAttribute(k_omega_apply_srht, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_omega_apply_srht<<<(unsigned)(c1 - c0 + 1), 256, smem, st>>>(
+    k_omega_apply_srht<<<dim3((unsigned)(c1 - c0 + 1), (unsigned)((m + kOaCols - 1) / kOaCols)), 256, smem, st>>>(
         Z, m, D.d, reinterpret_cast<const uint32_t*>(ws + L.off_tab),
         reinterpret_cast<const int32_t*>(ws + L.off_bucket_ofs), reinterpret_cast<const int32_t*>(ws + L.off_bucket_idx),
         D.seed, D.n, rb, re, c0, (float)(1.0 / std::sqrt((double)L.N)), X);
