@@ -315,16 +315,21 @@ __global__ void __launch_bounds__(1024) k_selection(uint64_t seed, int64_t N, in
   if (sact) perm[tid] = empty ? (erank < novf ? s_over[erank] : -1) : sv;
 }
 
-// Chunk signs of the sketch's gather: sgn[c][s] = (-1)^popc(c & a_t), t = perm[s], a_t = S_t / B; 0 for empty slots.
-__global__ void k_srht_signs(const int32_t* __restrict__ sel, const int32_t* __restrict__ perm, int d_pad, int A,
-                             float* __restrict__ sgn) {
+// Chunk signs of the sketch's gather, one byte per (chunk c, output group og): bit k set iff
+// (-1)^popc(c & a_t) = -1 for slot s = og*TPO + k, t = perm[s], a_t = S_t / B (empty slots: bit clear; their
+// accumulators are never stored).  A warp of the sketch reads its 16 groups' bytes as one 16-B sector.
+__global__ void k_srht_signs(const int32_t* __restrict__ sel, const int32_t* __restrict__ perm, int d_pad, int tpo,
+                             int A, uint8_t* __restrict__ sgnb) {
+  const int ng = d_pad / tpo;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= (int64_t)A * d_pad) return;
-  const int c = (int)(p / d_pad), sl = (int)(p - (int64_t)c * d_pad);
-  const int t = perm[sl];
-  float v = 0.f;
-  if (t >= 0) v = (__popc((uint32_t)c & ((uint32_t)sel[t] / (uint32_t)kSrhtB)) & 1) ? -1.f : 1.f;
-  sgn[p] = v;
+  if (p >= (int64_t)A * ng) return;
+  const int c = (int)(p / ng), og = (int)(p - (int64_t)c * ng);
+  uint32_t bits = 0;
+  for (int k = 0; k < tpo; ++k) {
+    const int t = perm[og * tpo + k];
+    if (t >= 0 && (__popc((uint32_t)c & ((uint32_t)sel[t] / (uint32_t)kSrhtB)) & 1)) bits |= 1u << k;
+  }
+  sgnb[p] = (uint8_t)bits;
 }
 
 
@@ -408,10 +413,11 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
                                            reinterpret_cast<int32_t*>(ws + L.off_bucket_idx),
                                            reinterpret_cast<int32_t*>(ws + L.off_perm));
     KS_LAUNCH_CHECK();
-    const int64_t ns = (int64_t)L.A * L.d_pad;
+    const int64_t ns = (int64_t)L.A * (L.d_pad / L.tpo);
     k_srht_signs<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(reinterpret_cast<const int32_t*>(ws + L.off_sel),
                                                                reinterpret_cast<const int32_t*>(ws + L.off_perm),
-                                                               L.d_pad, L.A, reinterpret_cast<float*>(ws + L.off_sgn));
+                                                               L.d_pad, L.tpo, L.A,
+                                                               reinterpret_cast<uint8_t*>(ws + L.off_sgn));
     KS_LAUNCH_CHECK();
   } else if (D.omega == KS_OMEGA_GAUSS) {
     dim3 grid((unsigned)((L.ncols_pad + 255) / 256), (unsigned)D.d);
@@ -473,7 +479,7 @@ KS_DEVINL void load_k32(f2_t (&kv)[16], const float* kr0, const float* kr1, int6
 template <int DIM, int KIND, int TPO>
 __global__ void __launch_bounds__(kSrhtThreads, 4)
 k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, const int32_t* __restrict__ perm,
-              const float* __restrict__ sgn, int64_t row_begin, int64_t row_end, int A, int d, int d_pad,
+              const uint8_t* __restrict__ sgnb, int64_t row_begin, int64_t row_end, int A, int d, int d_pad,
               float out_scale, float nugget, float* __restrict__ Y, const float* __restrict__ Kst, int64_t ldk,
               int64_t ncols) {
   extern __shared__ __align__(16) float Wbuf[];   // [2][kSrhtSmemFloats], chunk c uses half c & 1
@@ -586,10 +592,13 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
     }
     cp_async_wait_all();   // chunk c+1's points visible to all threads after the barrier
     __syncthreads();
-    // ---------------- phase C (the chunk's signs are L1-resident: one 4*d_pad-byte row per chunk)
+    // ---------------- phase C (the chunk's sign bits: one byte per output group, 64 bytes per chunk)
     float sg[TPO];
+    {
+      const uint32_t sb = __ldg(sgnb + (int64_t)c * (d_pad / TPO) + og);
 #pragma unroll
-    for (int k = 0; k < TPO; ++k) sg[k] = __ldg(sgn + (int64_t)c * d_pad + og * TPO + k);
+      for (int k = 0; k < TPO; ++k) sg[k] = __uint_as_float(((sb << (31 - k)) & 0x80000000u) | 0x3f800000u);
+    }
 #pragma unroll
     for (int k = 0; k < TPO; ++k) {
       const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(W + wofs[k]);
@@ -626,7 +635,7 @@ static ks_status launch_srht(const SketchLayout& L, const ks_sketch_desc& D, int
   kern<<<grid, kSrhtThreads, smem, st>>>(reinterpret_cast<const float4*>(ws + L.off_pk),
                                 reinterpret_cast<const int32_t*>(ws + L.off_sel),
                                 reinterpret_cast<const int32_t*>(ws + L.off_perm),
-                                reinterpret_cast<const float*>(ws + L.off_sgn), rb, re, L.A, D.d, L.d_pad,
+                                reinterpret_cast<const uint8_t*>(ws + L.off_sgn), rb, re, L.A, D.d, L.d_pad,
                                 (float)(1.0 / std::sqrt((double)L.N)), D.nugget, Y, sk ? sk->K : nullptr,
                                 sk ? sk->ldk : 0, D.n);
   KS_LAUNCH_CHECK();
