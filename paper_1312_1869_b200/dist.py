@@ -56,6 +56,20 @@ class CudaOps:
         self.k = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.qt_ws = _ws(ks_apply_qt_workspace_size(rows, d, self.m), self.device)
 
+    def stage_async(self, A_host):
+        """Host-resident (pinned) A: copied on a side stream so that the transfer overlaps the sketch and the
+        TSQR; returns the device buffer and the event the Q^T A step waits on."""
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+            self._A_dev = torch.empty(A_host.shape, dtype=torch.float32, device=self.device)
+        cur = torch.cuda.current_stream(self.device)
+        self._copy_stream.wait_stream(cur)   # the previous call's Q^T A has read the buffer
+        with torch.cuda.stream(self._copy_stream):
+            self._A_dev.copy_(A_host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(self._copy_stream)
+        return self._A_dev, ev
+
     def sketch(self, pts):
         """pts: the points (dim x n), or -- KS_KERNEL_STORED (NEXT-2) -- this rank's rows of K (rows x ldk)."""
         if self.desc.kernel == 2:
@@ -90,11 +104,21 @@ class CudaOps:
         return self.X
 
 
-def lowrank_solve_sharded(ops, pts, A_local, group=None):
+def lowrank_solve_sharded(ops, pts, A_local, group=None, X_host=None):
     """One pass of the row-sharded hot path; returns (X_local, Z, k, R).  With world size 1 the
-    collectives are skipped and the local TSQR is the whole factorisation."""
+    collectives are skipped and the local TSQR is the whole factorisation.
+
+    Host inputs (the end-to-end call): points on the host are copied first (the sketch needs them); a
+    host A (pinned) is copied on a side stream that overlaps the sketch and the TSQR (``ops.stage_async``);
+    ``X_host`` (pinned) receives X_local at the end."""
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
+    a_ready = None
+    on_gpu = getattr(ops, "device", torch.device("cpu")).type == "cuda"
+    if on_gpu and not pts.is_cuda:
+        pts = pts.to(ops.device, non_blocking=True)
+    if on_gpu and not A_local.is_cuda and hasattr(ops, "stage_async"):
+        A_local, a_ready = ops.stage_async(A_local)
     Y = ops.sketch(pts)
     Rp = ops.local_r(Y)
     if world > 1:
@@ -106,11 +130,15 @@ def lowrank_solve_sharded(ops, pts, A_local, group=None):
     else:
         R = Rp
         Q = ops.qform(None)
+    if a_ready is not None:
+        torch.cuda.current_stream(ops.device).wait_event(a_ready)
     Cm = ops.qt(Q, A_local)
     if world > 1:
         dist.all_reduce(Cm, op=dist.ReduceOp.SUM, group=group)
     Z, k = ops.trsolve(R, Cm)
     X = ops.omega_apply(Z)
+    if X_host is not None:
+        X_host.copy_(X, non_blocking=True)
     return X, Z, k, R
 
 
