@@ -220,10 +220,12 @@ def test_trsolve_hand_example_and_singular(ks, cuda):
     assert e.value.status == 2 and "index 1" in str(e.value)
 
 
-def test_apply_qt_and_apply_q(ks, cuda):
+# (5000, 96, 7): the generic split-K kernel (m % 4 != 0); the others the cp.async-staged k_qtx_fast with a
+# 32-column (m <= 32) or 64-column m tile, ragged d tiles (300 = 256 + 44), ragged rows and several chunks.
+@pytest.mark.parametrize("rows,d,m", [(5000, 96, 7), (5000, 96, 8), (3001, 300, 40), (70001, 512, 64)])
+def test_apply_qt_and_apply_q(ks, cuda, rows, d, m):
     import torch
     rng = np.random.default_rng(8)
-    rows, d, m = 5000, 96, 7
     Q = rng.standard_normal((rows, d)).astype(np.float32)
     X = rng.standard_normal((rows, m)).astype(np.float32)
     Cm = torch.empty((d, m), device=cuda)
@@ -236,10 +238,11 @@ def test_apply_qt_and_apply_q(ks, cuda):
     assert relF(Xo.cpu().numpy(), Q.astype(np.float64) @ Cm.cpu().numpy().astype(np.float64)) <= 1e-5
 
 
-@pytest.mark.parametrize("omega", [0, 1])
-def test_omega_apply_matches_oracle(ks, cuda, omega):
+# m = 40 / 64: the SRHT Omega-apply's 32-column tiles (a partial second tile / two full tiles)
+@pytest.mark.parametrize("omega,m", [(0, 5), (1, 5), (0, 40), (0, 64)])
+def test_omega_apply_matches_oracle(ks, cuda, omega, m):
     cfg, pts, A, prob = problem("c1", n=3000, d=64, omega=omega, dim=2)
-    Z = np.random.default_rng(1).standard_normal((64, 5)).astype(np.float32)
+    Z = np.random.default_rng(1).standard_normal((64, m)).astype(np.float32)
     sk = ks.Sketch(desc_of(cfg), cuda)
     X = sk.omega_apply(_t(Z, cuda)).cpu().numpy()
     Xr = prob.omega_apply(Z.astype(np.float64))
@@ -358,3 +361,20 @@ def test_trig_lowrank_solve_matches_oracle(ks, cuda, omega):
     _solve_parity(ks, cuda, cfg, pts, A, prob)
     cfg, pts, A, prob = problem("c2", omega=omega, n=6000, d=128, blocks=4)
     _solve_parity(ks, cuda, cfg, pts, A, prob)
+
+
+def test_host_inputs_match_device_inputs(ks, cuda):
+    """The end-to-end call (pinned host points / A, A's copy on a side stream, X copied back) gives the
+    same X as the device-resident call, bit for bit."""
+    import torch
+    from paper_1312_1869_b200 import dist as ksd
+    cfg, pts, A, prob = problem("c2", n=4096, blocks=4)
+    ops = ksd.CudaOps(desc_of(cfg), cfg["m"], cfg["blocks"], oracle.TAU, 0, 1, cuda)
+    X_dev = ksd.lowrank_solve_sharded(ops, _t(pts, cuda), _t(A, cuda))[0].clone()
+    torch.cuda.synchronize()
+    A_h = torch.as_tensor(A).pin_memory()
+    X_h = torch.empty((cfg["n"], cfg["m"]), dtype=torch.float32).pin_memory()
+    for _ in range(2):   # the second call reuses the staged A buffer
+        ksd.lowrank_solve_sharded(ops, torch.as_tensor(pts).pin_memory(), A_h, X_host=X_h)
+        torch.cuda.synchronize()
+        assert np.array_equal(X_h.numpy(), X_dev.cpu().numpy())
