@@ -746,7 +746,9 @@ __global__ void __launch_bounds__(256) k_omega_apply_srht(const float* __restric
   }
 }
 
-// Gaussian: X[j, :] = (1/sqrt d) sum_t Omega[j, t] Z[t, :].
+// Gaussian: X[j, :] = (1/sqrt d) sum_t Omega[j, t] Z[t, :].  Thread = row j, up to 32 columns per pass in
+// registers (one read of Omega^T per pass, coalesced across the rows of a warp), the t loop unrolled by 8 so
+// eight Omega loads are in flight together; Z broadcast from shared memory.
 __global__ void __launch_bounds__(256) k_omega_apply_gauss(const __half* __restrict__ omT, const __half* __restrict__ omT_lo,
                                                            int64_t ldo, const float* __restrict__ Z, int m, int d,
                                                            int64_t row_begin, int64_t row_end, float scale,
@@ -757,18 +759,48 @@ __global__ void __launch_bounds__(256) k_omega_apply_gauss(const __half* __restr
   const int64_t j = row_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= row_end) return;
   float* xr = X + (j - row_begin) * (int64_t)m;
-  for (int c0 = 0; c0 < m; c0 += 8) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int t = 0; t < d; ++t) {
-      float o = __half2float(omT[(int64_t)t * ldo + j]);
-      if (omT_lo) o += __half2float(omT_lo[(int64_t)t * ldo + j]);
+  for (int c0 = 0; c0 < m; c0 += 32) {
+    const int nc = min(32, m - c0);
+    float acc[32];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (c0 + q < m) acc[q] = fmaf(o, zs[t * m + c0 + q], acc[q]);
+    for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+    for (int t0 = 0; t0 < d; t0 += 8) {
+      float o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u;
+        o[u] = 0.f;
+        if (t < d) {
+          o[u] = __half2float(omT[(int64_t)t * ldo + j]);
+          if (omT_lo) o[u] += __half2float(omT_lo[(int64_t)t * ldo + j]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u;
+        if (t < d) {
+          const float* zr = zs + t * m + c0;
+          if ((m & 3) == 0) {   // 16-B aligned rows of Z: LDS.128 broadcasts
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4)
+              if (4 * q4 < nc) {
+                const float4 z = *reinterpret_cast<const float4*>(zr + 4 * q4);
+                acc[4 * q4 + 0] = fmaf(o[u], z.x, acc[4 * q4 + 0]);
+                acc[4 * q4 + 1] = fmaf(o[u], z.y, acc[4 * q4 + 1]);
+                acc[4 * q4 + 2] = fmaf(o[u], z.z, acc[4 * q4 + 2]);
+                acc[4 * q4 + 3] = fmaf(o[u], z.w, acc[4 * q4 + 3]);
+              }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q < nc) acc[q] = fmaf(o[u], zr[q], acc[q]);
+          }
+        }
+      }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (c0 + q < m) xr[c0 + q] = acc[q] * scale;
+    for (int q = 0; q < 32; ++q)
+      if (q < nc) xr[c0 + q] = acc[q] * scale;
   }
 }
 
