@@ -145,12 +145,8 @@ KS_API ks_status ks_omega_apply(const ks_sketch_desc* desc, const float* Z_dev, 
 typedef struct ks_tsqr_plan* ks_tsqr_handle;
 
 /* Merge topology of the block R's: the pairwise tree (eqs. (2)-(3), the default) or the chain of
- * eq. (5) (the running R absorbs one block R per step).  R is the same (unique).
- * KS_TSQR_STACKED: the input IS `blocks` stacked upper-triangular d x d matrices (rows == blocks * d;
- * entries below each block's diagonal are ignored) -- the all-gathered block R's of the multi-GPU second
- * level (eq. (5)'s final merge).  Their leaf QR is the identity, so only the merge runs
- * (one flat level of <= 16 blocks, then further levels); ks_tsqr_merge uses it. */
-typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1, KS_TSQR_STACKED = 2 } ks_tsqr_topology;
+ * eq. (5) (the running R absorbs one block R per step).  R is the same (unique). */
+typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1 } ks_tsqr_topology;
 
 KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks, size_t* bytes);
 KS_API ks_status ks_tsqr_workspace_size_ex(int64_t rows, int32_t d, int32_t blocks, int32_t topology, size_t* bytes);

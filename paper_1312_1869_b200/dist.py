@@ -30,7 +30,7 @@ class CudaOps:
     """The seven local steps through the C-ABI library (device tensors, current stream)."""
 
     def __init__(self, desc, m, blocks_per_rank, tau, rank, world, device):
-        from . import (TSQR_STACKED, Sketch, TsqrPlan, _desc, _ws, ks_apply_qt, ks_apply_qt_workspace_size, ks_omega_apply,
+        from . import (Sketch, TsqrPlan, _desc, _ws, ks_apply_qt, ks_apply_qt_workspace_size, ks_omega_apply,
                        ks_qform, ks_sketch, ks_trsolve, ks_tsqr)
         self._f = dict(apply_qt=ks_apply_qt, omega_apply=ks_omega_apply, qform=ks_qform, sketch=ks_sketch,
                        trsolve=ks_trsolve, tsqr=ks_tsqr)
@@ -43,8 +43,8 @@ class CudaOps:
         f32 = dict(dtype=torch.float32, device=self.device)
         self.sk = Sketch(self.desc, self.device)
         self.plan = TsqrPlan(rows, d, blocks_per_rank, self.device)
-        # the second level: one QR of the stacked triangular R's (no leaf QR needed)
-        self.mplan = TsqrPlan(world * d, d, world, self.device, topology=TSQR_STACKED) if world > 1 else None
+        # the second level: one QR of the stacked R's (a single block)
+        self.mplan = TsqrPlan(world * d, d, 1, self.device) if world > 1 else None
         self.Y = torch.empty((rows, d), **f32)
         self.Q = torch.empty((rows, d), **f32)
         self.Rp = torch.empty((d, d), **f32)

@@ -378,29 +378,3 @@ def test_host_inputs_match_device_inputs(ks, cuda):
         ksd.lowrank_solve_sharded(ops, torch.as_tensor(pts).pin_memory(), A_h, X_host=X_h)
         torch.cuda.synchronize()
         assert np.array_equal(X_h.numpy(), X_dev.cpu().numpy())
-
-
-@pytest.mark.parametrize("P,d", [(2, 64), (5, 100), (8, 512), (20, 64)])
-def test_tsqr_stacked_triangles_merge(ks, cuda, P, d):
-    """KS_TSQR_STACKED (the multi-GPU second level): P stacked upper-triangular d x d blocks,
-    no leaf QR; R vs the textbook Householder QR of the stack, Q2^T Q2 = I, Q2 R = stack."""
-    import torch
-    rng = np.random.default_rng(P * 1000 + d)
-    blocks = []
-    for p in range(P):
-        B = np.triu(rng.standard_normal((d, d)))
-        B[np.arange(d), np.arange(d)] = np.abs(B[np.arange(d), np.arange(d)]) + 1.0
-        blocks.append(B)
-    S = np.concatenate(blocks, 0).astype(np.float32)
-    plan = ks.TsqrPlan(P * d, d, P, cuda, topology=ks.TSQR_STACKED)
-    Q2 = torch.empty((P * d, d), device=cuda)
-    R = torch.empty((d, d), device=cuda)
-    ks.ks_tsqr(plan.h, _t(S, cuda), Q2, R)
-    torch.cuda.synchronize()
-    Rg = R.cpu().numpy().astype(np.float64)
-    Qg = Q2.cpu().numpy().astype(np.float64)
-    _, Rr = oracle.householder_qr(S.astype(np.float64), want_q=False)
-    assert relF(align_rows(Rg, Rr), Rr) <= R_TOL
-    assert np.all(np.tril(Rg, -1) == 0) and np.all(np.diag(Rg) >= 0)
-    assert np.linalg.norm(Qg.T @ Qg - np.eye(d)) <= 1e-4 * np.sqrt(d)
-    assert relF(Qg @ Rg, S) <= 1e-5
