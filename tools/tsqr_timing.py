@@ -39,7 +39,7 @@ for P in (1, 2, 4, 8):
     line = f"P={P} rows/rank={rows} d={d} blocks/rank={bpr}: factor {t_f:.2f} ms, factor+Q {t_fq:.2f} ms"
     if P > 1:
         Rs = torch.randn(P * d, d, device=dev).triu_()
-        mp = ks.TsqrPlan(P * d, d, P, dev)
+        mp = ks.TsqrPlan(P * d, d, 1, dev)   # as dist.py: one block of <= 512-row leaves, one flat merge
         Q2 = torch.empty(P * d, d, device=dev)
         t_m = timed(lambda: ks.ks_tsqr(mp.h, Rs, Q2, R))
         line += f", merge ({P * d}x{d}) {t_m:.2f} ms"
