@@ -28,8 +28,10 @@ def _gpu_sketch(ks, cfg, pts, cuda, rb=0, re=None):
 
 # ---------------------------------------------------------------- randomness
 @pytest.mark.parametrize("n,d,omega", [(2048, 64, 0), (3000, 100, 0), (16384, 128, 0), (100, 10, 0), (64, 64, 0),
-                                       (1000, 64, 1), (4096, 256, 1)])
+                                       (1000, 64, 1), (4096, 256, 1), (65536, 256, 1)])
 def test_randomness_bit_exact(ks, cuda, n, d, omega):
+    # (65536, 256, 1): the whole c3-sized Gaussian Omega (16.7 M fp16 values; exercises the fp32 fast path of
+    # k_gauss_omega and its fp64 fallback near fp16 rounding boundaries)
     cfg, pts, A, prob = problem("c1", n=n, d=d, omega=omega, dim=2, seed=1234 + n)
     sk = ks.Sketch(desc_of(cfg), cuda)
     s, S, g = sk.export(signs=True, sel=omega == 0, gauss=omega == 1)
