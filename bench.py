@@ -242,7 +242,7 @@ def run_ours(args, cfg, pts_np, A_np):
     rb, re = ksd.shard_rows(n, world, rank)
     desc = dict(n=n, dim=cfg["dim"], kernel=cfg["kernel"], sigma2=cfg["sigma2"], ell=cfg["ell"],
                 nugget=cfg["nugget"], d=d, seed=cfg["seed"], omega=cfg["omega"])
-    ops = ksd.CudaOps(desc, m, blocks, 1e-5, rank, world, dev)
+    ops = ksd.CudaOps(desc, m, blocks, 1e-5, rank, world, dev, inplace=True)   # sketch into the TSQR plan
     planted = bool(cfg.get("planted"))
     if planted:   # NEXT-2: this rank's rows of the stored K = E D E^T (generated once, outside the timing)
         from ks_inputs.planted import planted_K_device

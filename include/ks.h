@@ -159,6 +159,11 @@ KS_API ks_status ks_tsqr_create_ex(int64_t rows, int32_t d, int32_t blocks, int3
                             size_t ws_bytes, ks_tsqr_handle* out);
 KS_API ks_status ks_tsqr_destroy(ks_tsqr_handle h);
 
+/* The plan's working matrix (device, rows x d, row-major, inside the caller's workspace; valid until
+ * destroy).  ks_tsqr factors a copy of Y_dev in it; passing this pointer itself as Y_dev skips the copy
+ * (the sketch can be written there directly) -- Y is then overwritten by the factorisation. */
+KS_API ks_status ks_tsqr_work_matrix(ks_tsqr_handle h, float** W_dev);
+
 /* Factor Y (device, rows x d, not modified).  R_dev: d x d output.  If Q_dev is
  * non-NULL the explicit Q (rows x d, Q^T Q = I) is formed: Q-hat = Q^b_1 Q^b_2 ...
  * (eq. 4).  The implicit factors stay in the handle for ks_qform. */

@@ -20,7 +20,7 @@ import torch
 __all__ = [
     "KsError", "SketchDesc", "SQEXP", "MATERN32", "STORED", "ks_sketch_stored", "SRHT", "GAUSS", "DHT", "DCT", "lib", "library_path",
     "ks_sketch_workspace_size", "ks_sketch", "ks_omega_export", "ks_omega_apply",
-    "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr", "ks_qform", "TSQR_TREE", "TSQR_CHAIN",
+    "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr_work_matrix", "ks_tsqr", "ks_qform", "TSQR_TREE", "TSQR_CHAIN",
     "ks_tsqr_workspace_size_ex", "ks_tsqr_create_ex", "ks_tsqr_apply_qt", "ks_tsqr_apply_q",
     "ks_tsqr_merge_workspace_size", "ks_tsqr_merge", "ks_apply_qt_workspace_size", "ks_apply_qt",
     "ks_apply_q", "ks_trsolve", "ks_lowrank_workspace_size", "ks_lowrank_solve", "ks_last_error",
@@ -77,6 +77,7 @@ _SIGS = {
     "ks_tsqr_apply_qt": [_P, _P, _i32, _P, _P],
     "ks_tsqr_apply_q": [_P, _P, _i32, _P, _P],
     "ks_tsqr_destroy": [_P],
+    "ks_tsqr_work_matrix": [_P, _P],
     "ks_tsqr": [_P, _P, _P, _P, _P],
     "ks_qform": [_P, _P, _P, _P],
     "ks_tsqr_merge_workspace_size": [_i32, _i32, C.POINTER(_sz)],
@@ -218,6 +219,13 @@ def ks_tsqr_apply_q(h, Cmat, m, X, stream=None):
 
 def ks_tsqr_destroy(h):
     _check(lib().ks_tsqr_destroy(h))
+
+
+def ks_tsqr_work_matrix(h) -> int:
+    """Device address of the plan's working matrix (rows x d fp32); see include/ks.h."""
+    p = C.c_void_p()
+    _check(lib().ks_tsqr_work_matrix(h, C.byref(p)))
+    return int(p.value)
 
 
 def ks_tsqr(h, Y, Q, R, stream=None):
@@ -398,6 +406,13 @@ class TsqrPlan:
         self.ws = _ws(ks_tsqr_workspace_size_ex(rows, d, blocks, topology), device)
         self.h = ks_tsqr_create_ex(rows, d, blocks, topology, self.ws)
         self.device = torch.device(device)
+
+    def work_matrix(self):
+        """The plan's working matrix as a (rows x d) view of its workspace: a sketch written here is factored
+        in place by ks_tsqr(h, work_matrix, ...) (no input copy; overwritten by the factorisation)."""
+        off = ks_tsqr_work_matrix(self.h) - self.ws.data_ptr()
+        n = self.rows * self.d
+        return self.ws[off:off + 4 * n].view(torch.float32).view(self.rows, self.d)
 
     def __del__(self):
         h = getattr(self, "h", None)

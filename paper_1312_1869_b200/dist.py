@@ -29,7 +29,7 @@ def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
 class CudaOps:
     """The seven local steps through the C-ABI library (device tensors, current stream)."""
 
-    def __init__(self, desc, m, blocks_per_rank, tau, rank, world, device):
+    def __init__(self, desc, m, blocks_per_rank, tau, rank, world, device, inplace=False):
         from . import (Sketch, TsqrPlan, _desc, _ws, ks_apply_qt, ks_apply_qt_workspace_size, ks_omega_apply,
                        ks_qform, ks_sketch, ks_trsolve, ks_tsqr)
         self._f = dict(apply_qt=ks_apply_qt, omega_apply=ks_omega_apply, qform=ks_qform, sketch=ks_sketch,
@@ -45,7 +45,9 @@ class CudaOps:
         self.plan = TsqrPlan(rows, d, blocks_per_rank, self.device)
         # the second level: one QR of the stacked R's (a single block)
         self.mplan = TsqrPlan(world * d, d, 1, self.device) if world > 1 else None
-        self.Y = torch.empty((rows, d), **f32)
+        # inplace: the sketch goes straight into the TSQR plan's working matrix (no rows x d copy, one
+        # rows x d buffer less); Y is then consumed by the factorisation
+        self.Y = self.plan.work_matrix() if inplace else torch.empty((rows, d), **f32)
         self.Q = torch.empty((rows, d), **f32)
         self.Rp = torch.empty((d, d), **f32)
         self.Q2 = torch.empty((world * d, d), **f32)

@@ -380,3 +380,18 @@ def test_host_inputs_match_device_inputs(ks, cuda):
         ksd.lowrank_solve_sharded(ops, torch.as_tensor(pts).pin_memory(), A_h, X_host=X_h)
         torch.cuda.synchronize()
         assert np.array_equal(X_h.numpy(), X_dev.cpu().numpy())
+
+
+def test_inplace_sketch_into_tsqr_plan(ks, cuda):
+    """CudaOps(inplace=True): the sketch is written into the TSQR plan's working matrix (ks_tsqr_work_matrix)
+    and factored there without the input copy; R and X are bit-identical to the copying path."""
+    import torch
+    from paper_1312_1869_b200 import dist as ksd
+    cfg, pts, A, prob = problem("c2", n=4096, blocks=4)
+    outs = []
+    for inplace in (False, True):
+        ops = ksd.CudaOps(desc_of(cfg), cfg["m"], cfg["blocks"], oracle.TAU, 0, 1, cuda, inplace=inplace)
+        X, Z, k, R = ksd.lowrank_solve_sharded(ops, _t(pts, cuda), _t(A, cuda))
+        torch.cuda.synchronize()
+        outs.append((X.cpu().numpy().copy(), R.cpu().numpy().copy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

@@ -21,7 +21,7 @@ cfg, pts, A = ks_inputs.make_problem(a.config)
 dev = torch.device("cuda:0")
 desc = dict(n=cfg["n"], dim=cfg["dim"], kernel=cfg["kernel"], sigma2=cfg["sigma2"], ell=cfg["ell"],
             nugget=cfg["nugget"], d=cfg["d"], seed=cfg["seed"], omega=cfg["omega"])
-ops = ksd.CudaOps(desc, cfg["m"], cfg["blocks"], 1e-5, 0, 1, dev)
+ops = ksd.CudaOps(desc, cfg["m"], cfg["blocks"], 1e-5, 0, 1, dev, inplace=True)
 P = torch.as_tensor(pts, device=dev)
 Ad = torch.as_tensor(A, device=dev)
 for _ in range(a.warm + a.passes):
