@@ -146,7 +146,9 @@ typedef struct ks_tsqr_plan* ks_tsqr_handle;
 
 /* Merge topology of the block R's: the pairwise tree (eqs. (2)-(3), the default) or the chain of
  * eq. (5) (the running R absorbs one block R per step).  R is the same (unique). */
-typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1 } ks_tsqr_topology;
+/* KS_TSQR_MIXED: eq. (5) exactly as printed -- the blocks in two halves, a chain inside each half (advancing
+ * side by side), then one merge of the two chains' R's: the paper's "mixture of the strategies". */
+typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1, KS_TSQR_MIXED = 2 } ks_tsqr_topology;
 
 KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks, size_t* bytes);
 KS_API ks_status ks_tsqr_workspace_size_ex(int64_t rows, int32_t d, int32_t blocks, int32_t topology, size_t* bytes);

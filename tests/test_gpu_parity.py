@@ -118,15 +118,18 @@ def test_tsqr_random_matrix_matches_oracle(ks, cuda, rows, d, blocks):
     assert relF(Q @ R, Y) <= 1e-5
 
 
+@pytest.mark.parametrize("chains", [1, 2])
 @pytest.mark.parametrize("rows,d,blocks", [(4096, 64, 8), (6000, 100, 5), (16384, 128, 16)])
-def test_tsqr_chain_topology_matches_oracle_chain(ks, cuda, rows, d, blocks):
-    """PAPER.md eq. (5) chain topology: R equals the oracle's chain TSQR (and hence the tree's, R unique)."""
+def test_tsqr_chain_topology_matches_oracle_chain(ks, cuda, rows, d, blocks, chains):
+    """PAPER.md eq. (5): one chain (KS_TSQR_CHAIN) or, as printed, two chains advancing side by side and a
+    final merge of their R's (KS_TSQR_MIXED): R equals the oracle's chain TSQR with that many chains (and
+    hence the tree's, R unique)."""
     rng = np.random.default_rng(rows + 7 * d)
     Y = rng.standard_normal((rows, d)).astype(np.float32)
-    plan = ks.TsqrPlan(rows, d, blocks, cuda, topology=ks.TSQR_CHAIN)
+    plan = ks.TsqrPlan(rows, d, blocks, cuda, topology=ks.TSQR_CHAIN if chains == 1 else ks.TSQR_MIXED)
     Q, R = plan.factor(_t(Y, cuda))
     Q, R = Q.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
-    Rc = oracle.tsqr_chain(Y.astype(np.float64), blocks)
+    Rc = oracle.tsqr_chain(Y.astype(np.float64), blocks, chains)
     assert np.all(np.tril(R, -1) == 0) and np.all(np.diag(R) >= 0)
     assert relF(R, Rc) <= R_TOL
     assert np.linalg.norm(Q.T @ Q - np.eye(d)) <= 1e-4 * np.sqrt(d)
