@@ -101,7 +101,8 @@ def test_sketch_full_config_sampled_rows(ks, cuda, name, nrows):
 
 # ---------------------------------------------------------------- TSQR
 TSQR_CASES = [(2048, 64, 4), (16384, 128, 8), (4096, 256, 16), (8192, 512, 8), (3000, 100, 3), (700, 33, 5),
-              (512, 512, 1), (530, 512, 1), (40000, 64, 3)]   # (530, 512, 1): one 530-row leaf (512-thread QR)
+              (512, 512, 1), (530, 512, 1), (40000, 64, 3),   # (530, 512, 1): one 530-row leaf (512-thread QR)
+              (4096, 100, 8), (8192, 36, 16)]   # TMA leaf apply (512-row leaves) with a partial last panel (w = 4)
 
 
 @pytest.mark.parametrize("rows,d,blocks", TSQR_CASES)
