@@ -145,7 +145,7 @@ class OracleStep:
     that r x d sample -- all linear in the number of rows, so their time is scaled by n / r --
     plus the truncated back substitution and the full X = Omega Z once."""
 
-    def __init__(self, cfg, pts, A, budget_s=6.0, rows_hint=0, krows=None):
+    def __init__(self, cfg, pts, A, budget_s=6.0, rows_hint=0, krows=None, threads=None):
         import oracle
         self.oracle = oracle
         self.cfg = cfg
@@ -154,7 +154,7 @@ class OracleStep:
         _ = self.prob.s, self.prob.S  # randomness (setup, excluded like the GPU's)
         if cfg["omega"] == 1:
             _ = self.prob.om16
-        self.threads = oracle._threads()
+        self.threads = oracle._threads(threads)
         n, d = cfg["n"], cfg["d"]
         if rows_hint:
             rows = rows_hint
@@ -167,20 +167,32 @@ class OracleStep:
         self.rows = int(min(n, max(rows, d)))
         self.sel = np.linspace(0, n - 1, self.rows).astype(np.int64)
         self.A = np.asarray(A, np.float64)
-        self.sample = (f"oracle (fp64 C, {self.threads} threads): sketch of {self.rows} evenly spaced rows of Y, "
-                       f"TSQR with explicit Q and Q^T A of that {self.rows}x{d} sample, times n/{self.rows}; "
-                       f"truncated back substitution and the full X = Omega Z once")
+        self.extrapolated = self.rows < n
+        if self.extrapolated:
+            self.sample = (f"oracle (fp64 C, {self.threads} threads): sketch of {self.rows} evenly spaced rows of Y "
+                           f"({self.rows / n:.4f} of n), TSQR with explicit Q and Q^T A of that {self.rows}x{d} sample, "
+                           f"times n/{self.rows} (EXTRAPOLATED: rows are independent); truncated back substitution "
+                           f"and the full X = Omega Z once")
+        else:
+            self.sample = (f"oracle (fp64 C, {self.threads} threads): the whole step on the whole workload "
+                           f"(not extrapolated)")
+        self.last_measured_s = None
+
+    def info(self):
+        return {"cores": self.threads, "extrapolated": self.extrapolated, "sample_rows": self.rows,
+                "sample_fraction": self.rows / self.cfg["n"], "measured_s_per_step": self.last_measured_s}
 
     def _sketch(self, rows):
         if self.krows is not None:
             return self.prob.sketch_stored(self.krows(rows))
-        return self.prob.sketch_rows(rows)
+        return self.prob.sketch_rows(rows, nthreads=self.threads)
 
     def run(self):
         o, n = self.oracle, self.cfg["n"]
         t0 = time.perf_counter()
         Y = self._sketch(self.sel)
-        Q, R = o.tsqr_tree(Y, max(1, min(self.threads, self.rows // (2 * self.cfg['d']))), want_q=True)
+        Q, R = o.tsqr_tree(Y, max(1, min(self.threads, self.rows // (2 * self.cfg['d']))), want_q=True,
+                           nthreads=self.threads)
         Cm = o.matmul(np.ascontiguousarray(Q.T), self.A[self.sel])
         t_lin = time.perf_counter() - t0
         t1 = time.perf_counter()
@@ -188,6 +200,7 @@ class OracleStep:
         Z = o.back_substitute(R, Cm, k)
         self.prob.omega_apply(Z)
         t_once = time.perf_counter() - t1
+        self.last_measured_s = t_lin + t_once
         return t_lin * n / self.rows + t_once
 
     def value(self, seconds):
@@ -211,7 +224,10 @@ def run_reference(args, cfg, pts, A):
                     krows=planted_rows_fn(cfg) if cfg.get("planted") else None)
     for _ in range(max(0, min(args.warmup, 1))):
         st.run()
-    times = [st.run() for _ in range(args.steps)]
+    times, measured = [], []
+    for _ in range(args.steps):
+        times.append(st.run())
+        measured.append(st.last_measured_s)
     t = statistics.mean(times)
     v = st.value(t)
     print(json.dumps({
@@ -219,9 +235,12 @@ def run_reference(args, cfg, pts, A):
         "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (ks_inputs, Philox seeded)",
         "config": make_config(args.config, cfg, world),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": st.threads, "kind": "oracle", "sample": st.sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": st.threads, "kind": "oracle", "sample": st.sample,
+                         **st.info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+        "extrapolated": st.extrapolated,
+        "measured_s_per_step": statistics.mean(measured),
+    }), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
@@ -233,6 +252,8 @@ def run_ours(args, cfg, pts_np, A_np):
 
     rank, world, local = dist_env()
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
@@ -278,9 +299,8 @@ def run_ours(args, cfg, pts_np, A_np):
             sk_ev[2 * s + 1].record(stream)
             Rp = ops.local_r(Y)
             if world > 1:
-                Rstack = torch.empty((world * d, d), dtype=torch.float32, device=dev)
-                dist.all_gather_into_tensor(Rstack, Rp)
-                Q2, R = ops.merge(Rstack)
+                dist.all_gather_into_tensor(ops.Rstack, Rp)
+                Q2, R = ops.merge(ops.Rstack)
                 Q = ops.qform(Q2[rank * d:(rank + 1) * d].contiguous())
             else:
                 R = Rp
@@ -309,9 +329,8 @@ def run_ours(args, cfg, pts_np, A_np):
     e[0].record(stream); Y = ops.sketch(pts); e[1].record(stream)
     Rp = ops.local_r(Y)
     if world > 1:
-        Rstack = torch.empty((world * d, d), dtype=torch.float32, device=dev)
-        dist.all_gather_into_tensor(Rstack, Rp)
-        Q2, R = ops.merge(Rstack)
+        dist.all_gather_into_tensor(ops.Rstack, Rp)
+        Q2, R = ops.merge(ops.Rstack)
         Q = ops.qform(Q2[rank * d:(rank + 1) * d].contiguous())
     else:
         R = Rp
@@ -407,7 +426,11 @@ def run_ours(args, cfg, pts_np, A_np):
             st = OracleStep(cfg, pts_np, A_np, rows_hint=args.cpu_rows, krows=krows)
             t_or = st.run()
             cpu = {"value": st.value(t_or), "unit": UNIT, "cores": st.threads, "kind": "oracle",
-                   "sample": st.sample, "extrapolated_s_per_step": t_or}
+                   "sample": st.sample, "s_per_step": t_or, **st.info()}
+            st1 = OracleStep(cfg, pts_np, A_np, budget_s=4.0, krows=krows, threads=1)   # the same on 1 core
+            t1 = st1.run()
+            cpu["one_core"] = {"value": st1.value(t1), "unit": UNIT, "s_per_step": t1, "sample": st1.sample,
+                               **st1.info()}
         out = {
             "metric": METRIC,
             "value": n * n * d / (t_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -421,14 +444,41 @@ def run_ours(args, cfg, pts_np, A_np):
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": launches, "k": int(k.item()),
         }
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
+def relaunch_distributed(args):
+    """`--gpus N` (N > 1) outside torchrun: check the GPUs exist, then re-exec this command as N ranks under
+    torch.distributed.run (one process per GPU, NCCL).  Inside torchrun: WORLD_SIZE must equal N."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have}")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # the NCCL init lines show every rank joining
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execvpe(sys.executable, cmd, env)
+
+
 def main():
     args = parse()
+    relaunch_distributed(args)
     cfg = dict(ks_inputs.CONFIGS[args.config])
     cfg["seed"] = ks_inputs.config_seed(args.config)
     pts = None if cfg.get("planted") else ks_inputs.points(cfg["seed"], cfg["n"], cfg["dim"], cfg["dist"])

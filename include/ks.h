@@ -94,7 +94,7 @@ KS_API ks_status ks_sketch_workspace_size(const ks_sketch_desc* desc, size_t* by
 
 /* Y = rows [row_begin, row_end) of K Omega  (PAPER.md:95 "K-hat = K Omega", :19).
  *   pts_dev : device, fp32 SoA, dim x n (coordinate c of point j at pts[c*n + j])
- *   Y_dev   : device, fp32, (row_end - row_begin) x d, row-major
+ *   Y_dev   : device, fp32, (row_end - row_begin) x d, row-major, 16-byte aligned
  *   ws_dev  : device workspace of ks_sketch_workspace_size bytes (contents
  *             after the call: the sketch randomness, reused by ks_omega_apply)
  * Generates the randomness (signs, selection, Gaussian Omega) in the workspace,
@@ -154,7 +154,9 @@ KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks,
 KS_API ks_status ks_tsqr_workspace_size_ex(int64_t rows, int32_t d, int32_t blocks, int32_t topology, size_t* bytes);
 
 /* Create a plan over a caller-owned device workspace (kept until destroy).  _ex selects the topology
- * (KS_ERR_INVALID_ARGUMENT for an unknown one). */
+ * (KS_ERR_INVALID_ARGUMENT for an unknown one).  The plan metadata is copied into the workspace
+ * synchronously (no stream argument): the workspace must be idle -- no kernel queued on any stream may
+ * still be using it.  Plans are per device (create, run and destroy with the same current device). */
 KS_API ks_status ks_tsqr_create(int64_t rows, int32_t d, int32_t blocks, void* ws_dev, size_t ws_bytes,
                          ks_tsqr_handle* out);
 KS_API ks_status ks_tsqr_create_ex(int64_t rows, int32_t d, int32_t blocks, int32_t topology, void* ws_dev,
@@ -258,8 +260,10 @@ KS_API ks_status ks_gp_loglik(const float* U_dev, int64_t rows, int32_t r, const
                               const float* y_dev, double* out_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
 
 /* One-shot single-GPU path: sketch -> tsqr -> apply_qt -> trsolve -> omega_apply.
- *   A_dev n x m, X_dev n x m, Z_dev d x m, k_dev int32 (device).  Workspace
- *   size from ks_lowrank_workspace_size. */
+ *   A_dev n x m, X_dev n x m, Z_dev d x m, k_dev int32 (device, required: the truncation rank k < d is
+ *   how a caller detects that the solve was truncated).  Workspace size from ks_lowrank_workspace_size.
+ *   tau as in ks_trsolve: tau > 0 truncates (async); tau == 0 is the strict solve, which returns
+ *   KS_ERR_SINGULAR (naming the index) when some |r_jj| <= 1e-12 max|r_ii| and synchronises `stream`. */
 KS_API ks_status ks_lowrank_workspace_size(const ks_sketch_desc* desc, int32_t m, int32_t blocks, size_t* bytes);
 KS_API ks_status ks_lowrank_solve(const ks_sketch_desc* desc, const float* pts_dev, const float* A_dev, int32_t m,
                            int32_t blocks, float tau, float* X_dev, float* Z_dev, int32_t* k_dev, void* ws_dev,

@@ -59,6 +59,7 @@ def lib():
             "ko_fwht": (None, [P, i64]),
             "ko_omega_srht": (None, [P, P, i64, i64, i32, P]),
             "ko_matmul": (None, [P, P, i64, i64, i64, P]),
+            "ko_matmul_mt": (None, [P, P, i64, i64, i64, P, i]),
             "ko_sketch_srht_rows": (None, [P, i64, i, i, dbl, dbl, dbl, P, P, i64, i32, P, i64, P, i]),
             "ko_sketch_gauss_rows": (None, [P, i64, i, i, dbl, dbl, dbl, P, i32, P, i64, P, i]),
             "ko_householder_qr": (None, [P, i64, i32, P, P]),
@@ -195,6 +196,15 @@ def matmul(A: np.ndarray, B: np.ndarray) -> np.ndarray:
     B = np.ascontiguousarray(B, np.float64)
     Cm = np.zeros((A.shape[0], B.shape[1]))
     lib().ko_matmul(_p(A), _p(B), A.shape[0], A.shape[1], B.shape[1], _p(Cm))
+    return Cm
+
+
+def matmul_mt(A: np.ndarray, B: np.ndarray, nthreads=None) -> np.ndarray:
+    """ko_matmul with the rows of the product split over threads (the same sums in the same order)."""
+    A = np.ascontiguousarray(A, np.float64)
+    B = np.ascontiguousarray(B, np.float64)
+    Cm = np.zeros((A.shape[0], B.shape[1]))
+    lib().ko_matmul_mt(_p(A), _p(B), A.shape[0], A.shape[1], B.shape[1], _p(Cm), _threads(nthreads))
     return Cm
 
 
@@ -355,16 +365,16 @@ def lowrank_solve(prob: Problem, A: np.ndarray, blocks: int, tau: float = TAU, Y
     if Y is None:
         Y = prob.sketch_rows(nthreads=nthreads) if prob.n > 4096 else prob.sketch_tierA()
     Q, R = tsqr_tree(Y, blocks, want_q=True, nthreads=nthreads)
-    Cm = _qt_apply(Q, A64)
+    Cm = _qt_apply(Q, A64, nthreads)
     k = truncation_rank(R, tau)
     Z = back_substitute(R, Cm, k)
     X = prob.omega_apply(Z)
     return dict(Y=Y, Q=Q, R=R, C=Cm, k=k, Z=Z, X=X, rho=rho_profile(Cm, A64))
 
 
-def _qt_apply(Q: np.ndarray, A: np.ndarray) -> np.ndarray:
-    """C = Q^T A by the plain triple loop (ko_matmul on the transposed Q)."""
-    return matmul(np.ascontiguousarray(Q.T), A)
+def _qt_apply(Q: np.ndarray, A: np.ndarray, nthreads=None) -> np.ndarray:
+    """C = Q^T A by the plain triple loop (ko_matmul on the transposed Q; rows of C split over threads)."""
+    return matmul_mt(np.ascontiguousarray(Q.T), A, nthreads)
 
 
 def rho_of(Y: np.ndarray, Z: np.ndarray, A: np.ndarray) -> float:

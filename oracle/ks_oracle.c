@@ -448,27 +448,49 @@ typedef struct node {
   int64_t row0;           /* leaves: first row of the block */
 } node;
 
-typedef struct { const double* A; int64_t d; node* nd; } leaf_job;
-static void* leaf_worker(void* arg) {
-  leaf_job* L = (leaf_job*)arg;
+/* Independent QRs run in batches of up to nthreads threads (rows of different blocks are independent;
+ * results do not depend on the thread count). */
+typedef struct { const double* A; int64_t d; node* nd; } qr_job;
+static void* qr_worker(void* arg) {
+  qr_job* L = (qr_job*)arg;
   node* nd = L->nd;
-  ko_householder_qr(L->A + nd->row0 * L->d, nd->rows, (int32_t)L->d, nd->Qn, nd->R);
+  ko_householder_qr(L->A, nd->rows, (int32_t)L->d, nd->Qn, nd->R);
   return NULL;
 }
 
-static void qform_down(node* nd, const double* C, int32_t d, double* Q) {
-  /* this node's contribution: (Qn * C) distributed to its children / rows */
+static void run_qr_jobs(qr_job* jobs, int32_t cnt, int nthreads) {
+  for (int32_t i0 = 0; i0 < cnt; i0 += nthreads) {
+    int c = (cnt - i0) < nthreads ? (cnt - i0) : nthreads;
+    pthread_t th[64];
+    for (int t = 0; t < c; ++t) pthread_create(&th[t], NULL, qr_worker, &jobs[i0 + t]);
+    for (int t = 0; t < c; ++t) pthread_join(th[t], NULL);
+  }
+}
+
+/* eq. (4) top-down: the d x d factor C that multiplies each leaf's Qn (Q-hat rows of the leaf =
+ * Qn_leaf * C_leaf).  Internal nodes: (Qn_node * C) split into the children's d x d blocks. */
+static void qform_collect(node* nd, const double* C, int32_t d, double* Cleaf, node** leaves, int32_t* nleaf) {
+  if (nd->kid[0] == NULL) {
+    memcpy(Cleaf + (int64_t)(*nleaf) * d * d, C, sizeof(double) * (size_t)d * d);
+    leaves[(*nleaf)++] = nd;
+    return;
+  }
   double* QC = (double*)malloc(sizeof(double) * (size_t)(nd->rows * d));
   ko_matmul(nd->Qn, C, nd->rows, d, d, QC);
-  if (nd->kid[0] == NULL) {
-    memcpy(Q + nd->row0 * d, QC, sizeof(double) * (size_t)(nd->rows * d));
-  } else if (nd->kid[1] == NULL) {
-    qform_down(nd->kid[0], QC, d, Q);
+  if (nd->kid[1] == NULL) {
+    qform_collect(nd->kid[0], QC, d, Cleaf, leaves, nleaf);
   } else {
-    qform_down(nd->kid[0], QC, d, Q);
-    qform_down(nd->kid[1], QC + (int64_t)d * d, d, Q);
+    qform_collect(nd->kid[0], QC, d, Cleaf, leaves, nleaf);
+    qform_collect(nd->kid[1], QC + (int64_t)d * d, d, Cleaf, leaves, nleaf);
   }
   free(QC);
+}
+
+typedef struct { const double* Qn; const double* C; int64_t rows; int32_t d; double* out; } mm_job;
+static void* mm_worker(void* arg) {
+  mm_job* J = (mm_job*)arg;
+  ko_matmul(J->Qn, J->C, J->rows, J->d, J->d, J->out);
+  return NULL;
 }
 
 static void free_tree(node* nd) {
@@ -481,7 +503,11 @@ static void free_tree(node* nd) {
 /* returns 0, or -1 if some block has fewer than d rows (L13 / SPEC.md:235) */
 int ko_tsqr_tree(const double* A, int64_t m, int32_t d, int32_t b, double* R, double* Q, int nthreads) {
   if (b < 1 || m / b < d) return -1;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 64) nthreads = 64;
   node** level = (node**)malloc(sizeof(node*) * (size_t)b);
+  node** leaves = (node**)malloc(sizeof(node*) * (size_t)b);
+  qr_job* jobs = (qr_job*)malloc(sizeof(qr_job) * (size_t)b);
   for (int32_t i = 0; i < b; ++i) {
     node* nd = (node*)calloc(1, sizeof(node));
     int64_t r0 = (m * i) / b, r1 = (m * (i + 1)) / b;
@@ -489,50 +515,80 @@ int ko_tsqr_tree(const double* A, int64_t m, int32_t d, int32_t b, double* R, do
     nd->Qn = (double*)malloc(sizeof(double) * (size_t)(nd->rows * d));
     nd->R = (double*)malloc(sizeof(double) * (size_t)d * d);
     level[i] = nd;
+    jobs[i].A = A + r0 * d; jobs[i].d = d; jobs[i].nd = nd;
   }
-  /* eq. (1): independent leaf QRs (in batches of up to nthreads threads) */
-  if (nthreads < 1) nthreads = 1;
-  if (nthreads > 64) nthreads = 64;
-  for (int32_t i0 = 0; i0 < b; i0 += nthreads) {
-    int cnt = (b - i0) < nthreads ? (b - i0) : nthreads;
-    pthread_t th[64]; leaf_job jobs[64];
-    for (int t = 0; t < cnt; ++t) {
-      jobs[t].A = A; jobs[t].d = d; jobs[t].nd = level[i0 + t];
-      pthread_create(&th[t], NULL, leaf_worker, &jobs[t]);
-    }
-    for (int t = 0; t < cnt; ++t) pthread_join(th[t], NULL);
-  }
-  /* eqs. (2)-(3): pairwise QRs of stacked R's */
+  /* eq. (1): independent leaf QRs */
+  run_qr_jobs(jobs, b, nthreads);
+  /* eqs. (2)-(3): pairwise QRs of stacked R's, the pairs of one level independent */
   int32_t cnt = b;
   while (cnt > 1) {
     int32_t nxt = 0;
+    double** stk = (double**)malloc(sizeof(double*) * (size_t)(cnt / 2));
     for (int32_t i = 0; i + 1 < cnt; i += 2) {
       node* nd = (node*)calloc(1, sizeof(node));
       nd->rows = 2 * (int64_t)d;
       nd->kid[0] = level[i]; nd->kid[1] = level[i + 1];
-      double* stk = (double*)malloc(sizeof(double) * (size_t)(2 * d * d));
-      memcpy(stk, level[i]->R, sizeof(double) * (size_t)d * d);
-      memcpy(stk + (int64_t)d * d, level[i + 1]->R, sizeof(double) * (size_t)d * d);
+      double* st = (double*)malloc(sizeof(double) * (size_t)(2 * d * d));
+      memcpy(st, level[i]->R, sizeof(double) * (size_t)d * d);
+      memcpy(st + (int64_t)d * d, level[i + 1]->R, sizeof(double) * (size_t)d * d);
       nd->Qn = (double*)malloc(sizeof(double) * (size_t)(2 * d * d));
       nd->R = (double*)malloc(sizeof(double) * (size_t)d * d);
-      ko_householder_qr(stk, 2 * (int64_t)d, d, nd->Qn, nd->R);
-      free(stk);
+      stk[nxt] = st;
+      jobs[nxt].A = st; jobs[nxt].d = d; jobs[nxt].nd = nd;
       level[nxt++] = nd;
     }
+    run_qr_jobs(jobs, nxt, nthreads);
+    for (int32_t i = 0; i < nxt; ++i) free(stk[i]);
+    free(stk);
     if (cnt & 1) level[nxt++] = level[cnt - 1];        /* odd one passes through */
     cnt = nxt;
   }
   node* root = level[0];
   memcpy(R, root->R, sizeof(double) * (size_t)d * d);
   if (Q) {
+    /* eq. (4): Q-hat = Q^b_1 Q^b_2 ...: the node factors top-down, then Q rows of leaf i = Qn_i * C_i */
     double* I = (double*)calloc((size_t)d * d, sizeof(double));
     for (int32_t i = 0; i < d; ++i) I[i * d + i] = 1.0;
-    qform_down(root, I, d, Q);                         /* eq. (4): Q-hat = Q^b_1 Q^b_2 ... */
-    free(I);
+    double* Cleaf = (double*)malloc(sizeof(double) * (size_t)b * d * d);
+    int32_t nleaf = 0;
+    qform_collect(root, I, d, Cleaf, leaves, &nleaf);
+    mm_job* mj = (mm_job*)malloc(sizeof(mm_job) * (size_t)nleaf);
+    for (int32_t i0 = 0; i0 < nleaf; i0 += nthreads) {
+      int c = (nleaf - i0) < nthreads ? (nleaf - i0) : nthreads;
+      pthread_t th[64];
+      for (int t = 0; t < c; ++t) {
+        node* lf = leaves[i0 + t];
+        mj[i0 + t] = (mm_job){lf->Qn, Cleaf + (int64_t)(i0 + t) * d * d, lf->rows, d, Q + lf->row0 * d};
+        pthread_create(&th[t], NULL, mm_worker, &mj[i0 + t]);
+      }
+      for (int t = 0; t < c; ++t) pthread_join(th[t], NULL);
+    }
+    free(mj); free(Cleaf); free(I);
   }
   free_tree(root);
-  free(level);
+  free(level); free(leaves); free(jobs);
   return 0;
+}
+
+/* C (m x k) = A (m x p) B (p x k), the plain triple loop of ko_matmul with the rows of C split over
+ * threads (each element summed in the same order: identical to ko_matmul). */
+typedef struct { const double* A; const double* B; int64_t m0, m1, p, k; double* C; } mmr_job;
+static void* mmr_worker(void* arg) {
+  mmr_job* J = (mmr_job*)arg;
+  ko_matmul(J->A + J->m0 * J->p, J->B, J->m1 - J->m0, J->p, J->k, J->C + J->m0 * J->k);
+  return NULL;
+}
+
+void ko_matmul_mt(const double* A, const double* B, int64_t m, int64_t p, int64_t k, double* C, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 64) nthreads = 64;
+  if (nthreads > m) nthreads = (int)(m > 0 ? m : 1);
+  pthread_t th[64]; mmr_job J[64];
+  for (int t = 0; t < nthreads; ++t) {
+    J[t] = (mmr_job){A, B, (m * t) / nthreads, (m * (t + 1)) / nthreads, p, k, C};
+    pthread_create(&th[t], NULL, mmr_worker, &J[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
 }
 
 /* Chain scheme, eq. (5): each of `chains` contiguous groups

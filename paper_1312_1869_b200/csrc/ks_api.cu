@@ -51,6 +51,7 @@ extern "C" ks_status ks_sketch(const ks_sketch_desc* desc, const float* pts, int
   KS_TRY(sketch_validate(desc));
   KS_TRY(check_rows(desc, rb, re));
   if (!pts || !ws || (re > rb && !Y)) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if ((reinterpret_cast<uintptr_t>(Y) & 15) != 0) return fail(KS_ERR_INVALID_ARGUMENT, "Y must be 16-byte aligned");
   const SketchLayout L = sketch_layout(*desc);
   if (ws_bytes < L.bytes) return fail(KS_ERR_OOM, "sketch workspace too small: need " + std::to_string(L.bytes));
   char* w = static_cast<char*>(ws);
@@ -67,6 +68,7 @@ extern "C" ks_status ks_sketch_stored(const ks_sketch_desc* desc, const float* K
   KS_TRY(sketch_validate(desc));
   KS_TRY(check_rows(desc, rb, re));
   if (!K || !ws || (re > rb && !Y)) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if ((reinterpret_cast<uintptr_t>(Y) & 15) != 0) return fail(KS_ERR_INVALID_ARGUMENT, "Y must be 16-byte aligned");
   if (ldk < desc->n || (ldk & 3) != 0 || (reinterpret_cast<uintptr_t>(K) & 15) != 0)
     return fail(KS_ERR_INVALID_ARGUMENT, "need ldk >= n, ldk % 4 == 0 and a 16-byte aligned K");
   const SketchLayout L = sketch_layout(*desc);
@@ -267,7 +269,8 @@ extern "C" ks_status ks_lowrank_solve(const ks_sketch_desc* desc, const float* p
   LowrankLayout L;
   KS_TRY(lowrank_layout(desc, m, blocks, L));
   if (!pts || !A || !X || !Z || !ws) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
-  if (!(tau > 0.f)) return fail(KS_ERR_INVALID_ARGUMENT, "one-shot solve needs tau > 0");
+  if (!(tau >= 0.f) || !std::isfinite(tau)) return fail(KS_ERR_INVALID_ARGUMENT, "tau must be >= 0");
+  if (!k_dev) return fail(KS_ERR_INVALID_ARGUMENT, "k_dev is NULL (the truncation rank is the caller's signal)");
   if (ws_bytes < L.bytes) return fail(KS_ERR_OOM, "lowrank workspace too small: need " + std::to_string(L.bytes));
   char* w = static_cast<char*>(ws);
   const int64_t n = desc->n;
@@ -281,7 +284,7 @@ extern "C" ks_status ks_lowrank_solve(const ks_sketch_desc* desc, const float* p
   float* C = reinterpret_cast<float*>(w + L.off_C);
   KS_TRY(ks_sketch(desc, pts, 0, n, Y, w + L.off_sk, sk, stream));
   ks_tsqr_handle h = nullptr;
-  KS_TRY(ks_tsqr_create(n, d, blocks, w + L.off_tsqr, tsqr, &h));
+  KS_TRY(tsqr_create_on_stream(n, d, blocks, w + L.off_tsqr, tsqr, &h, S(stream)));
   tsqr_set_graphs(h, false);   // one-shot plan: capturing a graph would not pay off
   ks_status s = ks_tsqr(h, Y, Q, R, stream);
   ks_tsqr_destroy(h);

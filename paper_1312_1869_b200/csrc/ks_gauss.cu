@@ -495,12 +495,7 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   constexpr int NST = NB == 1 ? kG2Stages : 3;
   const int smem = 1024 + NST * (2 * kATileBytes + NB * (DN / 2) * kGaussBK * 2) + kPtsStages * kPtsBytes + 512;
   // split the column blocks in two when the row tiles leave a partial last wave (one CTA pair per 2 SMs)
-  static const int pair_slots = [] {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms / 2;
-  }();
+  const int pair_slots = num_sms() / 2;
   const int64_t pairs = (re - rb + 255) / 256;
   const int ksplit = (nkb >= 2 && pairs % pair_slots != 0 && pairs < 16 * pair_slots) ? 2 : 1;
   float* Y1 = reinterpret_cast<float*>(ws + L.off_ybuf);
@@ -515,7 +510,7 @@ static ks_status launch_gauss(const ks_sketch_desc& D, const SketchLayout& L, in
   KS_LAUNCH_CHECK();
   if (ksplit == 2) {
     const int64_t tot = (re - rb) * (int64_t)DN;
-    k_add_halves<<<(unsigned)std::min<int64_t>((tot / 4 + 255) / 256, 148 * 16), 256, 0, st>>>(
+    k_add_halves<<<(unsigned)std::min<int64_t>((tot / 4 + 255) / 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
         reinterpret_cast<float4*>(Y), reinterpret_cast<const float4*>(Y1), tot / 4);
     KS_LAUNCH_CHECK();
   }

@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
+#include <mutex>
 #include <string>
 
 #include "../../include/ks.h"
@@ -30,15 +32,43 @@ void add_launches(uint64_t n);   // kernels of a replayed CUDA graph
     KS_CUDA_TRY(cudaGetLastError());     \
   } while (0)
 
-// Streaming multiprocessors of the current device (persistent-grid sizing), queried once.
-inline int num_sms() {
-  static const int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v > 0 ? v : 148;
-  }();
-  return n;
+// Per-device state: every cached answer / one-time setup is keyed by the CURRENT device (a process may
+// drive several GPUs, from several host threads).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
 }
+
+// Streaming multiprocessors of the current device (persistent-grid sizing), cached per device.
+inline int num_sms() {
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  cache[dev].store(v, std::memory_order_relaxed);
+  return v;
+}
+
+// One-time per-device setup (e.g. cudaFuncSetAttribute, which is per device): runs f() once for each
+// device it is called on; thread-safe (a failed f() is retried on the next call).
+struct PerDeviceOnce {
+  std::atomic<bool> done[kMaxDevices];
+  std::mutex mu;
+  template <class F>
+  ks_status run(F&& f) {
+    const int dev = current_device();
+    if (done[dev].load(std::memory_order_acquire)) return KS_OK;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[dev].load(std::memory_order_relaxed)) return KS_OK;
+    const ks_status s = f();
+    if (s == KS_OK) done[dev].store(true, std::memory_order_release);
+    return s;
+  }
+};
 
 #define KS_TRY(expr)                     \
   do {                                   \
@@ -86,6 +116,9 @@ ks_status gauss_sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, in
 // ---------------------------------------------------------------- TSQR
 // Plans replay their launch sequence as a cached CUDA graph; one-shot plans switch that off.
 void tsqr_set_graphs(ks_tsqr_handle h, bool on);
+// ks_tsqr_create with the plan metadata uploaded stream-ordered on st (one-shot plans).
+ks_status tsqr_create_on_stream(int64_t rows, int32_t d, int32_t blocks, void* ws, size_t ws_bytes,
+                                ks_tsqr_handle* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- solve side
 // NEXT-4 (ks_gp.cu)

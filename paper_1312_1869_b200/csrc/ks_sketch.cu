@@ -398,11 +398,11 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
                                                  srht, reinterpret_cast<float4*>(ws + L.off_pk));
     KS_LAUNCH_CHECK();
   }
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  KS_TRY(attr.run([] {
     KS_CUDA_TRY(cudaFuncSetAttribute(k_selection, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelSmemBits / 8)));
-    attr = true;
-  }
+    return KS_OK;
+  }));
   const int sel_smem = L.N <= kSelSmemBits ? (int)((L.N + 31) / 32 * 4) : 0;
   if (srht) {
     k_selection<<<1, 1024, sel_smem, st>>>(D.seed, L.N, L.N, D.d, L.d_pad, L.tpo,

@@ -351,11 +351,11 @@ ks_status apply_q_run(const float* Q, int64_t rows, int d, const float* C, int m
 
 ks_status trsolve_run(const float* R, const float* C, int d, int m, float tau, float* Z, int32_t* k, cudaStream_t st) {
   if (d > kTrMaxD) return fail(KS_ERR_UNSUPPORTED, "trsolve supports d <= 1024");
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  KS_TRY(attr.run([] {
     KS_CUDA_TRY(cudaFuncSetAttribute(k_trsolve, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrSmem));
-    attr = true;
-  }
+    return KS_OK;
+  }));
   k_trsolve<<<(unsigned)((m + kTrMC - 1) / kTrMC), 256, kTrSmem, st>>>(R, C, d, m, tau, Z, k);
   KS_LAUNCH_CHECK();
   return KS_OK;

@@ -26,6 +26,32 @@ def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def _staged(t: torch.Tensor, group) -> bool:
+    """gloo cannot run every collective on CUDA tensors: stage them through host memory (the CPU tests
+    of the multi-rank path on one GPU; NCCL takes the device tensors directly)."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None):
+    """C1: out ((P d) x d) = the stacked R_p of every rank (NCCL all_gather over NVLink)."""
+    if _staged(inp, group):
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def all_reduce_sum(t: torch.Tensor, group=None):
+    """C2: t = sum over ranks (NCCL all_reduce)."""
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
 class CudaOps:
     """The seven local steps through the C-ABI library (device tensors, current stream)."""
 
@@ -51,6 +77,7 @@ class CudaOps:
         self.Q = torch.empty((rows, d), **f32)
         self.Rp = torch.empty((d, d), **f32)
         self.Q2 = torch.empty((world * d, d), **f32)
+        self.Rstack = torch.empty((world * d, d), **f32)   # C1's output, reused every call
         self.R = torch.empty((d, d), **f32)
         self.C = torch.empty((d, self.m), **f32)
         self.Z = torch.empty((d, self.m), **f32)
@@ -125,8 +152,10 @@ def lowrank_solve_sharded(ops, pts, A_local, group=None, X_host=None):
     Rp = ops.local_r(Y)
     if world > 1:
         d = Rp.shape[0]
-        Rstack = torch.empty((world * d, d), dtype=Rp.dtype, device=Rp.device)
-        dist.all_gather_into_tensor(Rstack, Rp.contiguous(), group=group)
+        Rstack = getattr(ops, "Rstack", None)
+        if Rstack is None:
+            Rstack = torch.empty((world * d, d), dtype=Rp.dtype, device=Rp.device)
+        all_gather_into(Rstack, Rp.contiguous(), group=group)
         Q2, R = ops.merge(Rstack)
         Q = ops.qform(Q2[rank * d:(rank + 1) * d].contiguous())
     else:
@@ -136,7 +165,7 @@ def lowrank_solve_sharded(ops, pts, A_local, group=None, X_host=None):
         torch.cuda.current_stream(ops.device).wait_event(a_ready)
     Cm = ops.qt(Q, A_local)
     if world > 1:
-        dist.all_reduce(Cm, op=dist.ReduceOp.SUM, group=group)
+        all_reduce_sum(Cm, group=group)
     Z, k = ops.trsolve(R, Cm)
     X = ops.omega_apply(Z)
     if X_host is not None:
@@ -153,7 +182,7 @@ def cond_diag_sharded(Y_local, R, group=None):
     G = torch.empty((d, d), dtype=torch.float32, device=Y_local.device)
     ks_cond_gram(Y_local, R, G, _ws(ks_cond_diag_workspace_size(rows, d), Y_local.device))
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
+        all_reduce_sum(G, group=group)
     out = torch.empty(4, dtype=torch.float32, device=Y_local.device)
     ks_cond_from_gram(G, out, _ws(1024 * d, Y_local.device))
     return out

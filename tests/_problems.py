@@ -22,11 +22,19 @@ def relF(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def align_rows(Rg, Rr):
-    """Row-sign alignment of R (= column signs of Q) where |r_jj| sits at the noise floor (L12)."""
+NOISE_FLOOR = 1e-6   # |r_jj| <= NOISE_FLOOR * max|r_ii|: the row's sign is not determined in fp32 (L12)
+
+
+def align_rows(Rg, Rr, floor=NOISE_FLOOR):
+    """Row-sign alignment of R (= column signs of Q), only for rows whose diagonal |r_jj| sits at the
+    noise floor (reading L12): r_jj >= 0 on both sides fixes every other row's sign, so a wrong-signed
+    healthy row is never flipped into agreement."""
     Rg = np.array(Rg, np.float64)
+    Rr = np.asarray(Rr, np.float64)
+    dr = np.abs(np.diag(Rr))
+    noisy = dr <= floor * dr.max()
     s = np.sign(np.sum(Rg * Rr, axis=1))
-    s[s == 0] = 1
+    s[(s == 0) | ~noisy] = 1
     return Rg * s[:, None]
 
 

@@ -7,6 +7,7 @@ X via rho(Z) = ||A - Y_ref Z||_F / ||A||_F within 1e-4 of rho_ref(k_gpu), |k_gpu
 import numpy as np
 import pytest
 
+import ks_inputs
 import oracle
 from _problems import align_rows, desc_of, problem, relF
 
@@ -399,3 +400,67 @@ def test_inplace_sketch_into_tsqr_plan(ks, cuda):
         torch.cuda.synchronize()
         outs.append((X.cpu().numpy().copy(), R.cpu().numpy().copy()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+# ---------------------------------------------------------------- exactly rank-deficient inputs
+def test_exact_rank16_K_through_pipeline(ks, cuda):
+    """The method's defining regime ("nearly rank deficient", range finder :95), exactly:
+    n = 2048 points at r = 16 distinct locations, no nugget, so rank(K) = 16 (SURVEY.md 8(c) end-to-end
+    pin; the oracle side is tests/test_oracle_qr_solve.py::test_exact_rank_recovery).  In fp32 the
+    trailing |r_jj| sit at the rounding floor (~1e-7 |r_11|), far below tau = 1e-5, while |r_16| / |r_11|
+    = 1.2e-3: the truncation rank is exactly 16, the first 16 columns of Q span range(K)
+    (||K - Q_16 Q_16^T K||_F / ||K||_F at fp32 rounding) and rho matches the oracle's rho_ref(16)."""
+    import torch
+    n, r, d, m = 2048, 16, 64, 4
+    loc = ks_inputs.points(21, r, 2)
+    pts = np.ascontiguousarray(loc[:, np.arange(n) % r])
+    desc = dict(n=n, dim=2, kernel=0, sigma2=1.0, ell=0.3, nugget=0.0, d=d, seed=21, omega=0)
+    A = ks_inputs.rhs(21, n, m)
+    pipe = ks.Pipeline(desc, m, 4, tau=oracle.TAU, device=cuda)
+    pipe(_t(pts, cuda), _t(A, cuda))
+    torch.cuda.synchronize()
+    kg = int(pipe.k.item())
+    assert kg == r, kg
+    prob = oracle.Problem(pts, oracle.SQEXP, 1.0, 0.3, 0.0, 21, d, 0)
+    K = prob.K_dense()
+    Q16 = pipe.Q.cpu().numpy().astype(np.float64)[:, :r]
+    resid = np.linalg.norm(K - Q16 @ (Q16.T @ K)) / np.linalg.norm(K)
+    assert resid <= 1e-5, resid
+    Zg = pipe.Z.cpu().numpy().astype(np.float64)
+    assert np.all(Zg[r:] == 0)
+    out = oracle.lowrank_solve(prob, A, 4)
+    assert out["k"] == r
+    assert abs(oracle.rho_of(out["Y"], Zg, A) - out["rho"][r]) <= RHO_TOL
+
+
+@pytest.mark.parametrize("zero_cols", [[5], list(range(40, 64)), [0, 1, 63]])
+def test_tsqr_exact_zero_columns(ks, cuda, zero_cols):
+    """Exactly rank-deficient Y (exact zero columns): the sigma = 0 Householder branch (no reflection,
+    r_jj = 0) in the leaves AND in every merge (a zero column stays exactly zero under reflections).  R is
+    unique only above the first deficient row (L12: compare what is unique, check the rest is valid):
+    rows < j0 against the oracle; r_jj == 0 exactly on the zero columns, R[:, zero] == 0; QR = Y and
+    Q^T Q = I everywhere; the strict solve (tau = 0) reports the singular index j0."""
+    import torch
+    rows, d = 4096, 64
+    Y = np.random.default_rng(9).standard_normal((rows, d)).astype(np.float32)
+    Y[:, zero_cols] = 0.0
+    plan = ks.TsqrPlan(rows, d, 8, cuda)
+    Q, R = plan.factor(_t(Y, cuda))
+    Qn, Rn = Q.cpu().numpy().astype(np.float64), R.cpu().numpy().astype(np.float64)
+    j0 = min(zero_cols)
+    assert np.all(Rn[:, zero_cols] == 0.0)
+    assert np.all(np.tril(Rn, -1) == 0) and np.all(np.diag(Rn) >= 0)
+    _, Rr = oracle.tsqr_tree(Y.astype(np.float64), 8, want_q=False)
+    if j0 > 0:
+        assert relF(Rn[:j0], Rr[:j0]) <= R_TOL
+    assert relF(Qn @ Rn, Y) <= 1e-5
+    assert np.linalg.norm(Qn.T @ Qn - np.eye(d)) <= 1e-4 * np.sqrt(d)
+    Cm = torch.ones((d, 2), device=cuda)
+    Z = torch.empty((d, 2), device=cuda)
+    k = torch.zeros(1, dtype=torch.int32, device=cuda)
+    with pytest.raises(ks.KsError) as e:
+        ks.ks_trsolve(R, Cm, d, 2, 0.0, Z, k)
+    assert e.value.status == 2 and f"index {j0}" in str(e.value)
+    ks.ks_trsolve(R, Cm, d, 2, oracle.TAU, Z, k)
+    torch.cuda.synchronize()
+    assert int(k.item()) == j0
