@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libks_b200.so")
 SOURCES = ["ks_api.cu", "ks_sketch.cu", "ks_gauss.cu", "ks_tsqr.cu", "ks_solve.cu", "ks_gp.cu"]
-HEADERS = ["ks_common.cuh", "ks_internal.h", "ks_tc.cuh", os.path.join("..", "..", "include", "ks.h")]
+HEADERS = ["ks_common.cuh", "ks_internal.h", "ks_tc.cuh", "ks_tsqr_tc.inc", os.path.join("..", "..", "include", "ks.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v", "-cudart", "static"]
