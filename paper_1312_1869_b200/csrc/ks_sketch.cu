@@ -569,6 +569,8 @@ k_sketch_srht(const float4* __restrict__ pk, const int32_t* __restrict__ sel, co
     }
     __syncthreads();
     // ---------------- phase B: pairs (b, b+16) packed for l bits 0-3, then bit 4 inside the pairs
+    // (measured: a row-pair form -- 64 threads, LDS.64 / STS.64, all five levels in registers -- halves the
+    // shared-memory instructions but is slower, c4 51.6 -> 55.3 ms, c5 811 -> 881 ms: half the warps idle)
     {
       float* wB = W + oB;
       f2_t u[16];
