@@ -67,3 +67,60 @@ def test_cond_diag_known_singular_values():
     c, eps, lo, hi = gp.cond_diag((Q * s) @ V.T, np.eye(d))           # singular values s -> s_max / s_min
     assert abs(c - 1.3 / 0.6) <= 1e-10 and abs(eps - (1.3 ** 2 - 1)) <= 1e-10
     assert abs(lo - 0.36) <= 1e-10 and abs(hi - 1.69) <= 1e-10
+
+
+# ---------------------------------------------------------------- the Nystrom core (second K pass)
+def test_kernel_rows_equals_the_c_oracle_K():
+    """oracle.gp.kernel_rows (numpy) = the C oracle's materialised K (itself pinned by Tables 1-2)."""
+    import ks_inputs
+    import oracle
+    for name, over in (("c2", dict(n=300, d=16)), ("c4", dict(n=257, d=16)), ("c5", dict(n=200, d=16))):
+        cfg, pts, A = ks_inputs.make_problem(name, **over)
+        prob = oracle.Problem.from_cfg(cfg, pts)
+        K = prob.K_dense()
+        rows = np.array([0, 5, 17, cfg["n"] - 1])
+        np.testing.assert_allclose(gp.kernel_rows(prob, rows), K[rows], rtol=1e-13, atol=1e-15)
+
+
+def test_core_loglik_is_the_dense_log_density():
+    n, d, s2 = 300, 24, 0.05
+    Q = _orth(n, d, 11)
+    G = np.random.default_rng(12).standard_normal((d, d))
+    B = G @ G.T
+    y = np.random.default_rng(13).standard_normal(n)
+    S = Q @ B @ Q.T + s2 * np.eye(n)
+    sign, ld = np.linalg.slogdet(S)
+    quad = y @ np.linalg.solve(S, y)
+    ll, q2, ld2 = gp.log_likelihood_core(Q, B, s2, y)
+    assert abs(ld2 - ld) <= 1e-10 * abs(ld) and abs(q2 - quad) <= 1e-10 * quad
+    assert abs(ll + 0.5 * (n * np.log(2 * np.pi) + ld + quad)) <= 1e-10 * abs(ll)
+    X = np.random.default_rng(14).standard_normal((n, 3))
+    np.testing.assert_allclose(gp.woodbury_core(Q, B, s2, X), np.linalg.solve(S, X), rtol=1e-9, atol=1e-12)
+    # the spectral form: B = V diag(lam) V^T, U = Q V gives the same likelihood through log_likelihood
+    lam, V = np.linalg.eigh(B)
+    ll_u = gp.log_likelihood(Q @ V, lam, s2, y)
+    assert abs(ll_u[0] - ll) <= 1e-10 * abs(ll)
+
+
+def test_nystrom_core_exact_for_exact_rank_K():
+    """n = 2048 points at 16 locations, no nugget (rank(K) = 16; the SURVEY 8(c) end-to-end case): with Q_16
+    spanning range(K) the Nystrom form is exact, Q B Q^T = K, and the core log-likelihood of K + s2 I equals the
+    dense log-density."""
+    import ks_inputs
+    import oracle
+    n, r, d = 2048, 16, 64
+    loc = ks_inputs.points(21, r, 2)
+    pts = np.ascontiguousarray(loc[:, np.arange(n) % r])
+    prob = oracle.Problem(pts, oracle.SQEXP, 1.0, 0.3, 0.0, 21, d, 0)
+    Q, R = oracle.tsqr_tree(prob.sketch_rows(), 4)
+    Q16 = Q[:, :r]
+    W, B = gp.nystrom_core(prob, Q16, block=500)
+    K = prob.K_dense()
+    np.testing.assert_allclose(W, K @ Q16, rtol=0, atol=1e-12 * np.abs(K).max())
+    assert np.linalg.norm(Q16 @ B @ Q16.T - K) <= 1e-10 * np.linalg.norm(K)
+    s2 = 0.01
+    y = ks_inputs.rhs(21, n, 1)[:, 0].astype(np.float64)
+    sign, ld = np.linalg.slogdet(K + s2 * np.eye(n))
+    quad = y @ np.linalg.solve(K + s2 * np.eye(n), y)
+    ll, q2, ld2 = gp.log_likelihood_core(Q16, B, s2, y)
+    assert abs(ld2 - ld) <= 1e-9 * abs(ld) and abs(q2 - quad) <= 1e-9 * quad
