@@ -259,6 +259,39 @@ KS_API ks_status ks_gp_woodbury_solve(const float* U_dev, int64_t rows, int32_t 
 KS_API ks_status ks_gp_loglik(const float* U_dev, int64_t rows, int32_t r, const float* lam_dev, float sigma2,
                               const float* y_dev, double* out_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
 
+/* The Nystrom core of the approximate spectral decomposition K ~ Q B Q^T ("approximate QR
+ * decompositions are useful in obtaining other approximate matrix decompositions, such as approximate spectral
+ * decompositions", citing Halko-Martinsson-Tropp's Alg. 5.3): a SECOND fused pass over K,
+ *   W = K Q          (n x d; K generated on the fly from the points as in ks_sketch, never stored; the
+ *                    tensor-core contraction of the Hartley / cosine path with Q split into fp16 hi + lo)
+ *   B = (Q^T W + W^T Q) / 2   (d x d, deterministic split-K Q^T-apply, symmetrised)
+ *   desc  : n, dim, kernel (SQEXP / MATERN32), sigma2, ell, nugget as for ks_sketch; d = Q's columns,
+ *           d % 16 == 0, 16 <= d <= 256; omega and seed are ignored.
+ *   pts_dev : device fp32 SoA dim x n;  Q_dev : device fp32 n x d row-major (all n rows, e.g. the TSQR Q),
+ *           16-byte aligned;  W_dev : device fp32 n x d output, 16-byte aligned;  B_dev : device fp32 d x d.
+ * Errors: INVALID_ARGUMENT (desc, NULL / misaligned pointers), UNSUPPORTED (d, stored kernel), OOM, CUDA. */
+KS_API ks_status ks_nystrom_workspace_size(const ks_sketch_desc* desc, size_t* bytes);
+KS_API ks_status ks_nystrom_core(const ks_sketch_desc* desc, const float* pts_dev, const float* Q_dev, float* W_dev,
+                                 float* B_dev, void* ws_dev, size_t ws_bytes, ks_stream_t stream);
+
+/* The Gaussian likelihood / solve of ks_gp_* with the core form Sigma = Q B Q^T + sigma2 I (Q rows x d with
+ * orthonormal columns, B d x d symmetric positive semidefinite, e.g. from ks_nystrom_core; sigma2 > 0):
+ *   ks_gp_loglik_core:   out_dev (device double[3]) = { log-likelihood, y^T Sigma^{-1} y, log det Sigma } with
+ *                        y^T Sigma^{-1} y = (y^T y - c^T c) / sigma2 + c^T (B + sigma2 I)^{-1} c, c = Q^T y, and
+ *                        log det Sigma = log det (B + sigma2 I) + (rows - d) log sigma2 (Woodbury and the
+ *                        determinant lemma on the d x d core: a Cholesky factorisation in fp64 on the GPU).
+ *   ks_gp_woodbury_core: Z_dev (rows x q) = Sigma^{-1} X = X / sigma2 + Q ((B + sigma2 I)^{-1} c - c / sigma2),
+ *                        c = Q^T X; X / Z device fp32 rows x q, Z may not alias X.
+ * Limits: d <= 256, q <= 64.  Workspace: ks_gp_core_workspace_size(rows, d, q) (q = 1 for the likelihood).
+ * Errors: INVALID_ARGUMENT (NULL pointers, sizes < 1, sigma2 <= 0), UNSUPPORTED (limits), OOM. */
+KS_API ks_status ks_gp_core_workspace_size(int64_t rows, int32_t d, int32_t q, size_t* bytes);
+KS_API ks_status ks_gp_loglik_core(const float* Q_dev, int64_t rows, int32_t d, const float* B_dev, float sigma2,
+                                   const float* y_dev, double* out_dev, void* ws_dev, size_t ws_bytes,
+                                   ks_stream_t stream);
+KS_API ks_status ks_gp_woodbury_core(const float* Q_dev, int64_t rows, int32_t d, const float* B_dev, float sigma2,
+                                     const float* X_dev, int32_t q, float* Z_dev, void* ws_dev, size_t ws_bytes,
+                                     ks_stream_t stream);
+
 /* One-shot single-GPU path: sketch -> tsqr -> apply_qt -> trsolve -> omega_apply.
  *   A_dev n x m, X_dev n x m, Z_dev d x m, k_dev int32 (device, required: the truncation rank k < d is
  *   how a caller detects that the solve was truncated).  Workspace size from ks_lowrank_workspace_size.

@@ -73,14 +73,21 @@ def kernel_rows(prob, rows) -> np.ndarray:
     return K
 
 
-def nystrom_core(prob, Q: np.ndarray, block: int = 1024):
-    """(W, B): W = K Q streamed over row blocks of K (never the whole n x n), B = (Q^T W + W^T Q) / 2."""
+def nystrom_core(prob, Q: np.ndarray, block: int = 512, nthreads: int | None = None):
+    """(W, B): W = K Q streamed over row blocks of K (never the whole n x n; independent blocks on host threads),
+    B = (Q^T W + W^T Q) / 2."""
+    import concurrent.futures as cf
+    import os
     Q = np.asarray(Q, np.float64)
     n = Q.shape[0]
     W = np.empty_like(Q)
-    for r0 in range(0, n, block):
+
+    def one(r0):
         rows = np.arange(r0, min(n, r0 + block))
         W[rows] = kernel_rows(prob, rows) @ Q
+
+    with cf.ThreadPoolExecutor(max_workers=nthreads or os.cpu_count() or 1) as ex:
+        list(ex.map(one, range(0, n, block)))
     B = Q.T @ W
     return W, 0.5 * (B + B.T)
 

@@ -27,6 +27,8 @@ __all__ = [
     "ks_version", "Sketch", "TsqrPlan", "Pipeline", "make_desc",
     "ks_cond_diag_workspace_size", "ks_cond_diag", "ks_cond_gram", "ks_cond_from_gram", "cond_diag",
     "ks_gp_workspace_size", "ks_gp_woodbury_solve", "ks_gp_loglik", "gp_woodbury_solve", "gp_loglik",
+    "ks_nystrom_workspace_size", "ks_nystrom_core", "ks_gp_core_workspace_size", "ks_gp_loglik_core",
+    "ks_gp_woodbury_core", "nystrom_core", "gp_loglik_core", "gp_woodbury_core",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -68,6 +70,11 @@ _SIGS = {
     "ks_gp_workspace_size": [_i64, _i32, _i32, C.POINTER(_sz)],
     "ks_gp_woodbury_solve": [_P, _i64, _i32, _P, _f32, _P, _i32, _P, _P, _sz, _P],
     "ks_gp_loglik": [_P, _i64, _i32, _P, _f32, _P, _P, _P, _sz, _P],
+    "ks_nystrom_workspace_size": [C.POINTER(SketchDesc), C.POINTER(_sz)],
+    "ks_nystrom_core": [C.POINTER(SketchDesc), _P, _P, _P, _P, _P, _sz, _P],
+    "ks_gp_core_workspace_size": [_i64, _i32, _i32, C.POINTER(_sz)],
+    "ks_gp_loglik_core": [_P, _i64, _i32, _P, _f32, _P, _P, _P, _sz, _P],
+    "ks_gp_woodbury_core": [_P, _i64, _i32, _P, _f32, _P, _i32, _P, _P, _sz, _P],
     "ks_omega_export": [C.POINTER(SketchDesc), _P, _P, _P, _P, _sz, _P],
     "ks_omega_apply": [C.POINTER(SketchDesc), _P, _i32, _i64, _i64, _P, _P, _sz, _P],
     "ks_tsqr_workspace_size": [_i64, _i32, _i32, C.POINTER(_sz)],
@@ -346,6 +353,63 @@ def gp_loglik(U, lam, sigma2, y, stream=None):
     out = torch.empty(3, dtype=torch.float64, device=U.device)
     ks_gp_loglik(U, lam, sigma2, y, out, ws, stream)
     return out
+
+
+# ------------------------------------------------------------ NEXT-4: the Nystrom core K ~ Q B Q^T
+def ks_nystrom_workspace_size(desc) -> int:
+    b = _sz(0)
+    _check(lib().ks_nystrom_workspace_size(C.byref(_desc(desc)), C.byref(b)))
+    return b.value
+
+
+def ks_nystrom_core(desc, pts, Q, W, B, ws, stream=None):
+    _check(lib().ks_nystrom_core(C.byref(_desc(desc)), _ptr(pts, torch.float32, "pts"), _ptr(Q, torch.float32, "Q"),
+                                 _ptr(W, torch.float32, "W"), _ptr(B, torch.float32, "B"), _ptr(ws),
+                                 ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def ks_gp_core_workspace_size(rows, d, q) -> int:
+    b = _sz(0)
+    _check(lib().ks_gp_core_workspace_size(int(rows), int(d), int(q), C.byref(b)))
+    return b.value
+
+
+def ks_gp_loglik_core(Q, B, sigma2, y, out, ws, stream=None):
+    _check(lib().ks_gp_loglik_core(_ptr(Q, torch.float32, "Q"), Q.shape[0], Q.shape[1], _ptr(B, torch.float32, "B"),
+                                   float(sigma2), _ptr(y, torch.float32, "y"), _ptr(out, torch.float64, "out"), _ptr(ws),
+                                   ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def ks_gp_woodbury_core(Q, B, sigma2, X, Z, ws, stream=None):
+    _check(lib().ks_gp_woodbury_core(_ptr(Q, torch.float32, "Q"), Q.shape[0], Q.shape[1], _ptr(B, torch.float32, "B"),
+                                     float(sigma2), _ptr(X, torch.float32, "X"), X.shape[1], _ptr(Z, torch.float32, "Z"),
+                                     _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def nystrom_core(desc, pts, Q, stream=None):
+    """(W, B): W = K Q (a second fused pass over K), B = Q^T K Q symmetrised (K ~ Q B Q^T)."""
+    D = _desc(desc)
+    ws = _ws(ks_nystrom_workspace_size(D), Q.device)
+    W = torch.empty_like(Q)
+    B = torch.empty((Q.shape[1], Q.shape[1]), dtype=torch.float32, device=Q.device)
+    ks_nystrom_core(D, pts, Q, W, B, ws, stream)
+    return W, B
+
+
+def gp_loglik_core(Q, B, sigma2, y, stream=None):
+    """Device double[3]: (log-likelihood, y^T Sigma^-1 y, log det Sigma), Sigma = Q B Q^T + sigma2 I."""
+    ws = _ws(ks_gp_core_workspace_size(Q.shape[0], Q.shape[1], 1), Q.device)
+    out = torch.empty(3, dtype=torch.float64, device=Q.device)
+    ks_gp_loglik_core(Q, B, sigma2, y, out, ws, stream)
+    return out
+
+
+def gp_woodbury_core(Q, B, sigma2, X, stream=None):
+    X2 = X if X.dim() == 2 else X.reshape(-1, 1)
+    ws = _ws(ks_gp_core_workspace_size(Q.shape[0], Q.shape[1], X2.shape[1]), Q.device)
+    Z = torch.empty_like(X2)
+    ks_gp_woodbury_core(Q, B, sigma2, X2, Z, ws, stream)
+    return Z.reshape(X.shape)
 
 
 # ------------------------------------------------------------ workspace bundles

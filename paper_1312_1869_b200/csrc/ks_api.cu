@@ -225,6 +225,72 @@ extern "C" ks_status ks_trsolve(const float* R, const float* C, int32_t d, int32
   KS_GUARD_END
 }
 
+// ---------------------------------------------------------------- NEXT-4: Nystrom core + core likelihood
+extern "C" ks_status ks_nystrom_workspace_size(const ks_sketch_desc* desc, size_t* bytes) {
+  KS_GUARD_BEGIN
+  if (!desc || !bytes) return fail(KS_ERR_INVALID_ARGUMENT, "NULL argument");
+  ks_sketch_desc D = *desc;
+  D.omega = KS_OMEGA_DHT;
+  KS_TRY(sketch_validate(&D));
+  return nystrom_ws(D, bytes);
+  KS_GUARD_END
+}
+
+extern "C" ks_status ks_nystrom_core(const ks_sketch_desc* desc, const float* pts, const float* Q, float* W, float* B,
+                                     void* ws, size_t ws_bytes, ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  if (!desc) return fail(KS_ERR_INVALID_ARGUMENT, "desc is NULL");
+  ks_sketch_desc D = *desc;
+  D.omega = KS_OMEGA_DHT;   // (Omega is the given Q; the desc's omega field is ignored)
+  if (D.kernel == KS_KERNEL_STORED) return fail(KS_ERR_UNSUPPORTED, "ks_nystrom_core evaluates K from points");
+  KS_TRY(sketch_validate(&D));
+  if (!pts || !Q || !W || !B || !ws) return fail(KS_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if (((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(W)) & 15) != 0)
+    return fail(KS_ERR_INVALID_ARGUMENT, "Q and W must be 16-byte aligned");
+  size_t need = 0;
+  KS_TRY(nystrom_ws(D, &need));
+  if (ws_bytes < need) return fail(KS_ERR_OOM, "nystrom workspace too small: need " + std::to_string(need));
+  return nystrom_run(D, pts, Q, W, B, static_cast<char*>(ws), S(stream));
+  KS_GUARD_END
+}
+
+extern "C" ks_status ks_gp_core_workspace_size(int64_t rows, int32_t d, int32_t q, size_t* bytes) {
+  KS_GUARD_BEGIN
+  if (!bytes || rows < 1 || d < 1 || q < 1) return fail(KS_ERR_INVALID_ARGUMENT, "invalid argument");
+  return gp_core_ws(rows, d, q, bytes);
+  KS_GUARD_END
+}
+
+static ks_status core_check(const float* Q, int64_t rows, int32_t d, const float* B, float s2, const float* X,
+                            int32_t q, size_t ws_bytes, const void* ws) {
+  if (!Q || !B || !X || !ws || rows < 1 || d < 1 || q < 1) return fail(KS_ERR_INVALID_ARGUMENT, "invalid argument");
+  if (d > 256 || q > 64) return fail(KS_ERR_UNSUPPORTED, "need d <= 256, q <= 64");
+  if (!(s2 > 0.f) || !std::isfinite(s2)) return fail(KS_ERR_INVALID_ARGUMENT, "sigma2 must be > 0");
+  size_t need = 0;
+  KS_TRY(gp_core_ws(rows, d, q, &need));
+  if (ws_bytes < need) return fail(KS_ERR_OOM, "gp core workspace too small: need " + std::to_string(need));
+  return KS_OK;
+}
+
+extern "C" ks_status ks_gp_loglik_core(const float* Q, int64_t rows, int32_t d, const float* B, float sigma2,
+                                       const float* y, double* out, void* ws, size_t ws_bytes, ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  KS_TRY(core_check(Q, rows, d, B, sigma2, y, 1, ws_bytes, ws));
+  if (!out) return fail(KS_ERR_INVALID_ARGUMENT, "out is NULL");
+  return gp_loglik_core_run(Q, rows, d, B, sigma2, y, out, static_cast<char*>(ws), S(stream));
+  KS_GUARD_END
+}
+
+extern "C" ks_status ks_gp_woodbury_core(const float* Q, int64_t rows, int32_t d, const float* B, float sigma2,
+                                         const float* X, int32_t q, float* Z, void* ws, size_t ws_bytes,
+                                         ks_stream_t stream) {
+  KS_GUARD_BEGIN
+  KS_TRY(core_check(Q, rows, d, B, sigma2, X, q, ws_bytes, ws));
+  if (!Z || Z == X) return fail(KS_ERR_INVALID_ARGUMENT, "Z is NULL or aliases X");
+  return gp_woodbury_core_run(Q, rows, d, B, sigma2, X, q, Z, static_cast<char*>(ws), S(stream));
+  KS_GUARD_END
+}
+
 // ---------------------------------------------------------------- one-shot
 namespace {
 struct LowrankLayout {

@@ -326,4 +326,243 @@ ks_status gp_loglik_run(const float* U, int64_t rows, int r, const float* lam, f
   return KS_OK;
 }
 
+
+// ------------------------------------------------------------------ NEXT-4: the Nystrom core and its likelihood
+// K ~ Q B Q^T with B = Q^T K Q (PAPER.md:25's "approximate spectral decompositions", HM11 Alg. 5.3): W = K Q
+// is a second fused pass over K on the tensor cores (dense_apply_run), B = Q^T W by the deterministic split-K
+// Q^T-apply, then symmetrised.
+__global__ void k_symmetrize(float* __restrict__ B, int d) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= d * d) return;
+  const int i = p / d, j = p - i * d;
+  if (j <= i) return;
+  const float v = 0.5f * (B[i * d + j] + B[j * d + i]);
+  B[i * d + j] = v;
+  B[j * d + i] = v;
+}
+
+struct NysLayout {
+  size_t off_dense, off_qt, bytes;
+};
+static NysLayout nys_layout(const ks_sketch_desc& D) {
+  NysLayout L{};
+  size_t off = 0, qt = 0;
+  auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
+  L.off_dense = take(dense_apply_ws(D));
+  apply_qt_ws(D.n, D.d, D.d, &qt);
+  L.off_qt = take(qt);
+  L.bytes = off;
+  return L;
+}
+
+ks_status nystrom_ws(const ks_sketch_desc& D, size_t* bytes) {
+  *bytes = nys_layout(D).bytes;
+  return KS_OK;
+}
+
+ks_status nystrom_run(const ks_sketch_desc& D, const float* pts, const float* Q, float* W, float* B, char* ws,
+                      cudaStream_t st) {
+  const NysLayout L = nys_layout(D);
+  KS_TRY(dense_apply_run(D, pts, Q, W, ws + L.off_dense, st));
+  KS_TRY(apply_qt_run(Q, D.n, D.d, W, D.d, B, ws + L.off_qt, st));
+  k_symmetrize<<<(unsigned)((D.d * D.d + 255) / 256), 256, 0, st>>>(B, D.d);
+  KS_LAUNCH_CHECK();
+  return KS_OK;
+}
+
+// One CTA (1024 threads), fp64: L L^T = B + s2 I by right-looking Cholesky in the workspace A (d x d, the
+// lower triangle; L2-resident, column j broadcast through shared memory), then Z = (B + s2 I)^{-1} C for the
+// q columns of C at once (forward / backward substitution, the right-hand sides in shared memory), and
+//   out[0] = log det (B + s2 I) = 2 sum log l_jj,  out[1 + c] = C[:, c]^T C[:, c],  out[1 + q + c] = C[:, c]^T Z[:, c].
+constexpr int kCholThreads = 1024;
+constexpr int kCoreMaxD = 256, kCoreMaxQ = 64;
+constexpr int kCoreSmem = (kCoreMaxD * kCoreMaxQ + kCoreMaxD + 64) * 8;
+__global__ void __launch_bounds__(kCholThreads, 1)
+k_core_chol_solve(const float* __restrict__ B, int d, float s2, double* __restrict__ A, const float* __restrict__ Cm,
+                  int q, float* __restrict__ Z, double* __restrict__ out) {
+  extern __shared__ double csm[];
+  double* rs = csm;                       // [d][q] right-hand sides -> solutions
+  double* col = rs + kCoreMaxD * kCoreMaxQ;
+  double* red = col + kCoreMaxD;          // [64]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int p = tid; p < d * d; p += kCholThreads) {
+    const int i = p / d, k = p - i * d;
+    if (k <= i) A[p] = (double)B[p] + (i == k ? (double)s2 : 0.0);
+  }
+  __syncthreads();
+  double logdet = 0.0;   // (thread 0)
+  for (int j = 0; j < d; ++j) {
+    if (tid == 0) {
+      const double l = sqrt(A[j * d + j]);
+      A[j * d + j] = l;
+      col[j] = l;
+      logdet += 2.0 * log(l);
+    }
+    __syncthreads();
+    const double lj = col[j];
+    for (int i = j + 1 + tid; i < d; i += kCholThreads) {
+      const double v = A[i * d + j] / lj;
+      A[i * d + j] = v;
+      col[i] = v;
+    }
+    __syncthreads();
+    for (int i = j + 1 + warp; i < d; i += kCholThreads / 32) {   // trailing update, row i by one warp
+      const double ci = col[i];
+      for (int k = j + 1 + lane; k <= i; k += 32) A[i * d + k] = fma(-ci, col[k], A[i * d + k]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) out[0] = logdet;
+  for (int p = tid; p < d * q; p += kCholThreads) rs[p] = (double)Cm[p];
+  __syncthreads();
+  for (int j = 0; j < d; ++j) {   // forward: u_j = r_j / l_jj, then r_i -= l_ij u_j (i > j)
+    const double ljj = A[j * d + j];
+    for (int c = tid; c < q; c += kCholThreads) rs[j * q + c] /= ljj;
+    __syncthreads();
+    for (int p = tid; p < (d - j - 1) * q; p += kCholThreads) {
+      const int i = j + 1 + p / q, c = p % q;
+      rs[i * q + c] = fma(-A[i * d + j], rs[j * q + c], rs[i * q + c]);
+    }
+    __syncthreads();
+  }
+  for (int j = d - 1; j >= 0; --j) {   // backward: z_j = r_j / l_jj, then r_k -= l_jk z_j (k < j)
+    const double ljj = A[j * d + j];
+    for (int c = tid; c < q; c += kCholThreads) rs[j * q + c] /= ljj;
+    __syncthreads();
+    for (int p = tid; p < j * q; p += kCholThreads) {
+      const int k = p / q, c = p % q;
+      rs[k * q + c] = fma(-A[j * d + k], rs[j * q + c], rs[k * q + c]);
+    }
+    __syncthreads();
+  }
+  for (int p = tid; p < d * q; p += kCholThreads) Z[p] = (float)rs[p];
+  // c^T c and c^T z per column, fixed-order block sums (warp shuffles, then the 32 warp sums)
+  for (int c = 0; c < q; ++c) {
+    for (int w = 0; w < 2; ++w) {
+      double v = 0.0;
+      for (int i = tid; i < d; i += kCholThreads) {
+        const double ci = (double)Cm[i * q + c];
+        v = fma(ci, w == 0 ? ci : rs[i * q + c], v);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      if (tid < 32) {
+        double u = red[tid];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+        if (tid == 0) out[1 + w * q + c] = u;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// u = z - c / s2 (fp32, d x q) for the core Woodbury solve X = B / s2 + Q u
+__global__ void k_core_u(const float* __restrict__ Z, const float* __restrict__ C, int n, float s2,
+                         float* __restrict__ U) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) U[p] = Z[p] - C[p] / s2;
+}
+
+// y^T y in fp64 over fixed blocks, then out = {loglik, quad, logdet} from the core sums
+__global__ void __launch_bounds__(256) k_core_loglik(const float* __restrict__ y, int64_t n, int d, float s2,
+                                                     const double* __restrict__ core, double* __restrict__ part,
+                                                     unsigned* __restrict__ ticket, double* __restrict__ out) {
+  __shared__ double red[8];
+  __shared__ bool last;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+    s = fma((double)y[i], (double)y[i], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < 8; ++w) b += red[w];
+    part[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double yy = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) yy += ((volatile double*)part)[b];
+  const double quad = (yy - core[1]) / (double)s2 + core[2];
+  const double ld = core[0] + (double)(n - d) * log((double)s2);
+  out[0] = -0.5 * ((double)n * log(2.0 * 3.14159265358979323846) + ld + quad);
+  out[1] = quad;
+  out[2] = ld;
+  *ticket = 0u;
+}
+
+struct CoreLayout {
+  size_t off_c, off_z, off_u, off_core, off_a, off_qt, off_part, off_ticket, bytes;
+};
+static CoreLayout core_layout(int64_t rows, int d, int q) {
+  CoreLayout L{};
+  size_t off = 0, qt = 0;
+  auto take = [&](size_t b) { size_t o = off; off = align_up(off + b, 256); return o; };
+  L.off_c = take(sizeof(float) * (size_t)d * q);
+  L.off_z = take(sizeof(float) * (size_t)d * q);
+  L.off_u = take(sizeof(float) * (size_t)d * q);
+  L.off_core = take(sizeof(double) * (1 + 2 * (size_t)q));
+  L.off_a = take(sizeof(double) * (size_t)d * d);
+  apply_qt_ws(rows, d, q, &qt);
+  L.off_qt = take(qt);
+  L.off_part = take(sizeof(double) * kLlBlocks);
+  L.off_ticket = take(sizeof(unsigned));
+  L.bytes = off;
+  return L;
+}
+
+ks_status gp_core_ws(int64_t rows, int d, int q, size_t* bytes) {
+  *bytes = core_layout(rows, d, q).bytes;
+  return KS_OK;
+}
+
+static ks_status core_solve(const float* Q, int64_t rows, int d, const float* B, float s2, const float* X, int q,
+                            char* ws, cudaStream_t st, const CoreLayout& L) {
+  if (d > kCoreMaxD) return fail(KS_ERR_UNSUPPORTED, "core solve supports d <= 256");
+  if (q > kCoreMaxQ) return fail(KS_ERR_UNSUPPORTED, "core solve supports q <= 64");
+  float* C = reinterpret_cast<float*>(ws + L.off_c);
+  KS_TRY(apply_qt_run(Q, rows, d, X, q, C, ws + L.off_qt, st));   // C = Q^T X
+  static PerDeviceOnce attr;
+  KS_TRY(attr.run([] {
+    KS_CUDA_TRY(cudaFuncSetAttribute(k_core_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kCoreSmem));
+    return KS_OK;
+  }));
+  k_core_chol_solve<<<1, kCholThreads, kCoreSmem, st>>>(B, d, s2, reinterpret_cast<double*>(ws + L.off_a), C, q,
+                                                        reinterpret_cast<float*>(ws + L.off_z),
+                                                        reinterpret_cast<double*>(ws + L.off_core));
+  KS_LAUNCH_CHECK();
+  return KS_OK;
+}
+
+ks_status gp_loglik_core_run(const float* Q, int64_t rows, int d, const float* B, float s2, const float* y, double* out,
+                             char* ws, cudaStream_t st) {
+  const CoreLayout L = core_layout(rows, d, 1);
+  KS_TRY(core_solve(Q, rows, d, B, s2, y, 1, ws, st, L));
+  unsigned* ticket = reinterpret_cast<unsigned*>(ws + L.off_ticket);
+  KS_CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
+  k_core_loglik<<<kLlBlocks, 256, 0, st>>>(y, rows, d, s2, reinterpret_cast<const double*>(ws + L.off_core),
+                                           reinterpret_cast<double*>(ws + L.off_part), ticket, out);
+  KS_LAUNCH_CHECK();
+  return KS_OK;
+}
+
+ks_status gp_woodbury_core_run(const float* Q, int64_t rows, int d, const float* B, float s2, const float* X, int q,
+                               float* Z, char* ws, cudaStream_t st) {
+  const CoreLayout L = core_layout(rows, d, q);
+  KS_TRY(core_solve(Q, rows, d, B, s2, X, q, ws, st, L));
+  float* U = reinterpret_cast<float*>(ws + L.off_u);
+  k_core_u<<<(unsigned)((d * q + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float*>(ws + L.off_z),
+                                                          reinterpret_cast<const float*>(ws + L.off_c), d * q, s2, U);
+  KS_LAUNCH_CHECK();
+  return apply_q_run(Q, rows, d, U, q, Z, st, X, 1.f / s2, 1.f);   // Z = X / s2 + Q u
+}
+
 }  // namespace ks

@@ -113,6 +113,11 @@ ks_status omega_export_run(const ks_sketch_desc& desc, const SketchLayout& L, in
 ks_status gauss_sketch_run(const ks_sketch_desc& desc, const SketchLayout& L, int64_t row_begin,
                            int64_t row_end, float* Y, char* ws, cudaStream_t st, const StoredK* sk);
 
+// NEXT-4: W = K Om for a dense given Om (n x d, row-major), workspace dense_apply_ws(desc)
+ks_status dense_apply_run(const ks_sketch_desc& D, const float* pts, const float* Om, float* W, char* ws,
+                          cudaStream_t st);
+size_t dense_apply_ws(const ks_sketch_desc& D);
+
 // ---------------------------------------------------------------- TSQR
 // Plans replay their launch sequence as a cached CUDA graph; one-shot plans switch that off.
 void tsqr_set_graphs(ks_tsqr_handle h, bool on);
@@ -132,6 +137,14 @@ ks_status gp_woodbury_run(const float* U, int64_t rows, int r, const float* lam,
                           float* X, char* ws, cudaStream_t st);
 ks_status gp_loglik_run(const float* U, int64_t rows, int r, const float* lam, float s2, const float* y, double* out,
                         char* ws, cudaStream_t st);
+ks_status nystrom_ws(const ks_sketch_desc& D, size_t* bytes);
+ks_status nystrom_run(const ks_sketch_desc& D, const float* pts, const float* Q, float* W, float* B, char* ws,
+                      cudaStream_t st);
+ks_status gp_core_ws(int64_t rows, int d, int q, size_t* bytes);
+ks_status gp_loglik_core_run(const float* Q, int64_t rows, int d, const float* B, float s2, const float* y, double* out,
+                             char* ws, cudaStream_t st);
+ks_status gp_woodbury_core_run(const float* Q, int64_t rows, int d, const float* B, float s2, const float* X, int q,
+                               float* Z, char* ws, cudaStream_t st);
 ks_status apply_qt_ws(int64_t rows, int d, int m, size_t* bytes);
 ks_status apply_qt_run(const float* Q, int64_t rows, int d, const float* X, int m, float* C, void* ws,
                        cudaStream_t st);

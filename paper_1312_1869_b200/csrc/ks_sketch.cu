@@ -440,6 +440,57 @@ ks_status sketch_prepare(const ks_sketch_desc& D, const SketchLayout& L, const f
   return KS_OK;
 }
 
+// ============================================================ NEXT-4: K times a dense given matrix
+// W = K Om for a caller-given dense Om (n x d fp32, row-major -- e.g. the sketch's Q, the second pass over K
+// of the Nystrom core B = Q^T K Q): the tensor-core contraction of the Hartley / cosine path (NB = 2: Om
+// as fp16 hi + lo planes, x sqrt(n) like the trig planes) with the planes transposed from Om in 32 x 32
+// tiles (coalesced reads and writes).
+__global__ void k_dense_omega(const float* __restrict__ Om, int64_t n, int d, int64_t ncols_pad, float scale,
+                              __half* __restrict__ hi, __half* __restrict__ lo) {
+  __shared__ float tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32;
+  const int t0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {   // rows j0 + r, columns t0 + threadIdx.x of Om
+    const int64_t j = j0 + r;
+    const int t = t0 + threadIdx.x;
+    tile[r][threadIdx.x] = (j < n && t < d) ? Om[j * d + t] * scale : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {   // plane row t0 + r, columns j0 + threadIdx.x
+    const int t = t0 + r;
+    const int64_t j = j0 + threadIdx.x;
+    if (t < d && j < ncols_pad) {
+      const float v = tile[threadIdx.x][r];
+      const __half h = __float2half_rn(v);
+      hi[(int64_t)t * ncols_pad + j] = h;
+      lo[(int64_t)t * ncols_pad + j] = __float2half_rn(v - __half2float(h));
+    }
+  }
+}
+
+ks_status dense_apply_run(const ks_sketch_desc& D0, const float* pts, const float* Om, float* W, char* ws,
+                          cudaStream_t st) {
+  ks_sketch_desc D = D0;
+  D.omega = KS_OMEGA_DHT;   // the layout / launch of the two-plane tensor-core path
+  const SketchLayout L = sketch_layout(D);
+  const int64_t nb = (L.ncols_pad + 255) / 256;
+  k_pack_points<<<(unsigned)nb, 256, 0, st>>>(pts, D.n, D.dim, L.ncols_pad, coord_scale(D),
+                                               (float)(D.sigma2 * gauss_scale(D)), D.seed, 0,
+                                               reinterpret_cast<float4*>(ws + L.off_pk));
+  KS_LAUNCH_CHECK();
+  __half* hi = reinterpret_cast<__half*>(ws + L.off_gauss);
+  k_dense_omega<<<dim3((unsigned)((L.ncols_pad + 31) / 32), (unsigned)((D.d + 31) / 32)), dim3(32, 8), 0, st>>>(
+      Om, D.n, D.d, L.ncols_pad, (float)std::sqrt((double)D.n), hi, hi + (size_t)D.d * L.ncols_pad);
+  KS_LAUNCH_CHECK();
+  return gauss_sketch_run(D, L, 0, D.n, W, ws, st, nullptr);
+}
+
+size_t dense_apply_ws(const ks_sketch_desc& D0) {
+  ks_sketch_desc D = D0;
+  D.omega = KS_OMEGA_DHT;
+  return sketch_layout(D).bytes;
+}
+
 // ============================================================ fused SRHT kernel
 // One CTA = 8 rows of Y (128 threads, 4 CTAs per SM, whose phases interleave); loops over the column
 // chunks c of K.  The tile W is double buffered, so a chunk needs 2 barriers (after phase A, after B).

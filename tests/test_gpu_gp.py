@@ -114,3 +114,90 @@ def test_cond_split_api_matches_one_call(ks, cuda):
     out = out.cpu().numpy()
     c, eps, lo, hi = gp.cond_diag(Y.cpu().numpy(), R.cpu().numpy())
     assert abs(out[0] - one[0]) <= 1e-5 and abs(out[0] - c) <= 1e-4
+
+
+# ---------------------------------------------------------------- the Nystrom core K ~ Q B Q^T (second K pass)
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_nystrom_core_and_core_loglik_match_oracle(ks, cuda, name):
+    """Full c2 / c3: the pipeline's Q, then W = K Q on the tensor cores (ks_nystrom_core), B = Q^T W, and the
+    core-form likelihood / Woodbury solve (Sigma = Q B Q^T + s2 I, fp64 Cholesky of B + s2 I on the GPU) against
+    oracle/gp.py: (a) the same steps in fp64 from the GPU's Q ("given Q"): W, B <= 1e-5, log-likelihood and
+    Woodbury solve <= 1e-6 / 1e-5; (b) the whole oracle path (its own sketch, TSQR Q, Nystrom core and
+    likelihood): log-likelihood within 1e-5 relative (the north_star Y / R tolerances carried through)."""
+    import torch
+    cfg, pts, A, prob = problem(name)
+    n, d = cfg["n"], cfg["d"]
+    pipe = ks.Pipeline(desc_of(cfg), cfg["m"], cfg["blocks"], tau=oracle.TAU, device=cuda)
+    pipe(_t(pts, cuda), _t(A, cuda))
+    Q = pipe.Q
+    W, B = ks.nystrom_core(desc_of(cfg), _t(pts, cuda), Q)
+    s2 = 0.01
+    y = _t(A[:, 0], cuda)
+    ll = ks.gp_loglik_core(Q, B, s2, y)
+    Zw = ks.gp_woodbury_core(Q, B, s2, _t(A[:, :4], cuda))
+    torch.cuda.synchronize()
+    Qn = Q.cpu().numpy().astype(np.float64)
+    Wg, Bg = W.cpu().numpy(), B.cpu().numpy()
+    assert np.array_equal(Bg, Bg.T)
+    Wr, Br = gp.nystrom_core(prob, Qn)
+    assert relF(Wg, Wr) <= 1e-5, relF(Wg, Wr)
+    assert relF(Bg, Br) <= 1e-5, relF(Bg, Br)
+    llg = ll.cpu().numpy()
+    llr = gp.log_likelihood_core(Qn, Bg.astype(np.float64), s2, A[:, 0].astype(np.float64))
+    for a, b in zip(llg, llr):
+        assert abs(a - b) <= 1e-6 * abs(b), (llg, llr)
+    Zr = gp.woodbury_core(Qn, Bg.astype(np.float64), s2, A[:, :4].astype(np.float64))
+    assert relF(Zw.cpu().numpy(), Zr) <= 1e-5
+    # (b) the whole path in the oracle
+    out = oracle.lowrank_solve(prob, A, cfg["blocks"])
+    _, Bo = gp.nystrom_core(prob, out["Q"])
+    llo = gp.log_likelihood_core(out["Q"], Bo, s2, A[:, 0].astype(np.float64))
+    assert abs(llg[0] - llo[0]) <= 1e-5 * abs(llo[0]), (llg, llo)
+    print(f"{name}: W relF {relF(Wg, Wr):.2e}  B relF {relF(Bg, Br):.2e}  loglik gpu {llg[0]:.8e} oracle {llo[0]:.8e}")
+
+
+def test_core_loglik_exact_rank_K(ks, cuda):
+    """n = 2048 points at 16 locations, no nugget (rank(K) = 16): with the GPU's Q_16 the Nystrom core is exact
+    (Q B Q^T = K) and the core log-likelihood of K + s2 I equals the dense fp64 log-density."""
+    import torch
+    import ks_inputs
+    n, r, d = 2048, 16, 64
+    loc = ks_inputs.points(21, r, 2)
+    pts = np.ascontiguousarray(loc[:, np.arange(n) % r])
+    desc = dict(n=n, dim=2, kernel=0, sigma2=1.0, ell=0.3, nugget=0.0, d=d, seed=21, omega=0)
+    pipe = ks.Pipeline(desc, 4, 4, tau=oracle.TAU, device=cuda)
+    pipe(_t(pts, cuda), _t(ks_inputs.rhs(21, n, 4), cuda))
+    Q16 = pipe.Q[:, :r].contiguous()
+    desc16 = dict(desc, d=r)
+    W, B = ks.nystrom_core(desc16, _t(pts, cuda), Q16)
+    y = ks_inputs.rhs(21, n, 1)[:, 0]
+    ll = ks.gp_loglik_core(Q16, B, 0.01, _t(y, cuda))
+    torch.cuda.synchronize()
+    prob = oracle.Problem(pts, oracle.SQEXP, 1.0, 0.3, 0.0, 21, d, 0)
+    K = prob.K_dense()
+    Qn, Bn = Q16.cpu().numpy().astype(np.float64), B.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(Qn @ Bn @ Qn.T - K) <= 1e-5 * np.linalg.norm(K)
+    S = K + 0.01 * np.eye(n)
+    sign, ld = np.linalg.slogdet(S)
+    quad = y.astype(np.float64) @ np.linalg.solve(S, y.astype(np.float64))
+    llg = ll.cpu().numpy()
+    assert abs(llg[2] - ld) <= 1e-5 * abs(ld) and abs(llg[1] - quad) <= 1e-5 * quad, (llg, ld, quad)
+
+
+def test_core_argument_errors(ks, cuda):
+    import torch
+    Q = torch.zeros((100, 16), device=cuda)
+    B = torch.zeros((16, 16), device=cuda)
+    y = torch.zeros(100, device=cuda)
+    out = torch.empty(3, dtype=torch.float64, device=cuda)
+    ws = torch.empty(ks.ks_gp_core_workspace_size(100, 16, 1), dtype=torch.uint8, device=cuda)
+    with pytest.raises(ks.KsError) as e:
+        ks.ks_gp_loglik_core(Q, B, 0.0, y, out, ws)
+    assert e.value.status == 1
+    with pytest.raises(ks.KsError) as e:
+        ks.ks_gp_loglik_core(Q, B, 0.1, y, out, ws[:8])
+    assert e.value.status == 4
+    with pytest.raises(ks.KsError) as e:   # d = 40 is not a multiple of 16 (the tensor-core pass)
+        ks.nystrom_core(dict(n=100, dim=1, kernel=0, sigma2=1.0, ell=0.1, nugget=0.0, d=40, seed=1, omega=0),
+                        torch.zeros((1, 100), device=cuda), torch.zeros((100, 40), device=cuda))
+    assert e.value.status == 5
