@@ -61,7 +61,9 @@ def kernel_rows(prob, rows) -> np.ndarray:
     """K[rows, :] in fp64 (sigma2 kappa(r) + nugget on the diagonal by index, r by direct differences)."""
     rows = np.asarray(rows, np.int64)
     x = prob.pts.astype(np.float64)
-    r2 = ((x[:, rows, None] - x[:, None, :]) ** 2).sum(0)
+    r2 = np.zeros((rows.shape[0], x.shape[1]))
+    for c in range(x.shape[0]):          # r^2 = sum_c (x_ic - x_jc)^2 by direct differences (L10)
+        r2 += (x[c, rows, None] - x[c, None, :]) ** 2
     if prob.kind == 0:        # squared exponential, exp(-r^2 / (2 ell^2))   (L7)
         K = prob.sigma2 * np.exp(-r2 / (2.0 * prob.ell ** 2))
     elif prob.kind == 1:      # Matern-3/2, (1 + sqrt3 r / ell) exp(-sqrt3 r / ell)   (L8)
