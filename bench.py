@@ -345,6 +345,28 @@ def run_ours(args, cfg, pts_np, A_np):
     torch.cuda.synchronize(dev)
     ph = {"sketch": e[0].elapsed_time(e[1]), "tsqr_qform": e[1].elapsed_time(e[2]), "solve": e[2].elapsed_time(e[3])}
 
+    # implicit-Q variant (world size 1): the same step without forming Q (row a6), C = Q-hat^T A from the stored
+    # reflectors -- reported beside the contract step, not instead of it
+    implicit = None
+    if world == 1 and not planted:
+        ti = []
+        for s in range(args.steps + 1):
+            flush.fill_(s & 0xFF)
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            Y = ops.sketch(pts)
+            R = ops.local_r(Y)
+            Cm = ops.qt_implicit(A_loc)
+            Z, k_i = ops.trsolve(R, Cm)
+            ops.omega_apply(Z)
+            b.record(stream)
+            b.synchronize()
+            if s > 0:
+                ti.append(a.elapsed_time(b))
+        t_i = statistics.mean(ti)
+        implicit = {"ms_per_step": t_i, "value": n * n * d / (t_i * 1e-3), "unit": UNIT,
+                    "what": "sketch + TSQR (R only) + implicit Q^T A + trsolve + Omega Z: row a6 skipped"}
+
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if planted and n > 10000:
@@ -442,7 +464,7 @@ def run_ours(args, cfg, pts_np, A_np):
             "sketch_n2d_per_s": n * rows_per_gpu * d * world / (t_sk * 1e-3),
             "sketch_ms": t_sk, "solve_ms": t_step, "phase_ms": ph,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-            "gpu_launches": launches, "k": int(k.item()),
+            "gpu_launches": launches, "k": int(k.item()), "implicit_q": implicit,
         }
         print(json.dumps(out), flush=True)
     if world > 1:

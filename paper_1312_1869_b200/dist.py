@@ -124,6 +124,16 @@ class CudaOps:
         self._f["apply_qt"](Q, Q.shape[0], Q.shape[1], A, self.m, self.C, self.qt_ws)
         return self.C
 
+    def qt_implicit(self, A):
+        """C = Q-hat^T A from the stored reflectors (no explicit Q; NEXT-3): A is copied into a
+        work buffer that the reflectors overwrite (world size 1: the whole factorisation is local)."""
+        from . import ks_tsqr_apply_qt
+        if getattr(self, "_Xw", None) is None:
+            self._Xw = torch.empty((self.re - self.rb, self.m), dtype=torch.float32, device=self.device)
+        self._Xw.copy_(A)
+        ks_tsqr_apply_qt(self.plan.h, self._Xw, self.m, self.C)
+        return self.C
+
     def trsolve(self, R, Cm):
         self._f["trsolve"](R, Cm, R.shape[0], self.m, self.tau, self.Z, self.k)
         return self.Z, self.k
@@ -148,7 +158,10 @@ def lowrank_solve_sharded(ops, pts, A_local, group=None, X_host=None):
         pts = pts.to(ops.device, non_blocking=True)
     if on_gpu and not A_local.is_cuda and hasattr(ops, "stage_async"):
         A_local, a_ready = ops.stage_async(A_local)
+    nvtx = torch.cuda.nvtx if on_gpu else None
+    if nvtx: nvtx.range_push("ks.sketch")
     Y = ops.sketch(pts)
+    if nvtx: nvtx.range_pop(); nvtx.range_push("ks.tsqr")
     Rp = ops.local_r(Y)
     if world > 1:
         d = Rp.shape[0]
@@ -163,6 +176,7 @@ def lowrank_solve_sharded(ops, pts, A_local, group=None, X_host=None):
         Q = ops.qform(None)
     if a_ready is not None:
         torch.cuda.current_stream(ops.device).wait_event(a_ready)
+    if nvtx: nvtx.range_pop(); nvtx.range_push("ks.solve")
     Cm = ops.qt(Q, A_local)
     if world > 1:
         all_reduce_sum(Cm, group=group)
@@ -170,6 +184,7 @@ def lowrank_solve_sharded(ops, pts, A_local, group=None, X_host=None):
     X = ops.omega_apply(Z)
     if X_host is not None:
         X_host.copy_(X, non_blocking=True)
+    if nvtx: nvtx.range_pop()
     return X, Z, k, R
 
 
