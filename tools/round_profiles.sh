@@ -17,7 +17,7 @@ NCU="ncu --clock-control none --set full --import-source on"
 timeout 900 $NCU -k regex:k_sketch_srht -c 1 -o $out/srht_c4 python tools/profile_step.py c4 --warm 0 > $out/ncu1.log 2>&1
 timeout 900 $NCU -k regex:k_sketch_srht -c 1 -o $out/srht_c5 python tools/profile_step.py c5 --warm 0 > $out/ncu2.log 2>&1
 timeout 900 $NCU -k regex:k_sketch_gauss -c 1 -o $out/gauss_c3 python tools/profile_step.py c3 --warm 0 > $out/ncu3.log 2>&1
-KS_TSQR_GRAPH=0 timeout 900 $NCU -k regex:k_panel_apply_tma -c 1 -o $out/apply_leaf python tools/tsqr_one.py > $out/ncu4.log 2>&1
+KS_TSQR_GRAPH=0 timeout 900 $NCU -k regex:k_leaf_apply_tc -c 1 -o $out/apply_leaf python tools/tsqr_one.py > $out/ncu4.log 2>&1
 KS_TSQR_GRAPH=0 timeout 900 $NCU -k regex:k_panel_qr -c 1 -o $out/panel_qr python tools/tsqr_one.py > $out/ncu5.log 2>&1
 KS_TSQR_GRAPH=0 timeout 900 $NCU -k regex:k_qtx_fast -c 1 -o $out/qtx python tools/profile_step.py c4 --warm 0 > $out/ncu6.log 2>&1
 echo "done" >> $out/summary.txt

@@ -11,7 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 lib_path = os.path.join(ROOT, "paper_1312_1869_b200", "libks_b200.so")
 shutil.copy(lib_path, "/tmp/ks_keep.so")
-shutil.copy(sys.argv[1], lib_path)
+shutil.copy(sys.argv[1], lib_path + ".tmp")
+os.replace(lib_path + ".tmp", lib_path)   # a new inode: never rewrite a mapped library in place
 try:
     import torch
     import paper_1312_1869_b200 as ks
@@ -43,4 +44,5 @@ try:
     print(f"pass-1 waits per item (us): conv-slot / MMA done + drain {wv[:, 0].mean() / 1e3:.2f}, ring full {wv[:, 1].mean() / 1e3:.2f}")
     print("items per CTA:", np.bincount(valid.sum(1))[np.bincount(valid.sum(1)) > 0], "(counts of CTAs by items)")
 finally:
-    shutil.copy("/tmp/ks_keep.so", lib_path)
+    shutil.copy("/tmp/ks_keep.so", lib_path + ".tmp")
+    os.replace(lib_path + ".tmp", lib_path)
