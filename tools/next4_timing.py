@@ -46,6 +46,19 @@ def main():
     wsb = torch.empty(ks.ks_gp_workspace_size(n, d, B.shape[1]), dtype=torch.uint8, device=dev)
     X = torch.empty_like(B)
     res["gp_woodbury_ms_m%d" % B.shape[1]] = timed(lambda: ks.ks_gp_woodbury_solve(Q, lam, 1e-2, B, X, wsb))
+    if d <= 256 and d % 16 == 0:   # the Nystrom core (second K pass on the tensor cores) and the core likelihood
+        pts_d = torch.as_tensor(pts, device=dev)
+        wsn = torch.empty(ks.ks_nystrom_workspace_size(desc), dtype=torch.uint8, device=dev)
+        W = torch.empty_like(Q)
+        Bc = torch.empty((d, d), dtype=torch.float32, device=dev)
+        res["nystrom_core_ms"] = timed(lambda: ks.ks_nystrom_core(desc, pts_d, Q, W, Bc, wsn))
+        # tensor-pipe FLOPs of W = K Q: 2 n^2 d per product, 3 products (K_hi Q_hi, K_lo Q_hi, K_hi Q_lo)
+        res["nystrom_tensor_tflops"] = 3 * 2.0 * n * n * d / (res["nystrom_core_ms"] * 1e-3) / 1e12
+        wsc = torch.empty(ks.ks_gp_core_workspace_size(n, d, 1), dtype=torch.uint8, device=dev)
+        res["gp_loglik_core_ms"] = timed(lambda: ks.ks_gp_loglik_core(Q, Bc, 1e-2, y, o3, wsc))
+        res["loglik_core"] = float(o3[0].cpu())
+        wsw = torch.empty(ks.ks_gp_core_workspace_size(n, d, B.shape[1]), dtype=torch.uint8, device=dev)
+        res["gp_woodbury_core_ms_m%d" % B.shape[1]] = timed(lambda: ks.ks_gp_woodbury_core(Q, Bc, 1e-2, B, X, wsw))
     print(json.dumps(res))
 
 
