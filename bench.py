@@ -441,6 +441,13 @@ def run_ours(args, cfg, pts_np, A_np):
         if tr:
             roof["traffic"] = tr["traffic_bytes"]
             roof["traffic_source"] = f"{os.path.relpath(TRAFFIC_PATH, ROOT)} ({tr['kernel']})"
+            if tr.get("smem_wavefronts") and roof["bound"] == "alu":
+                # the SRHT sketch's binding datapath: shared-memory wavefronts per launch (ncu)
+                # over the measured sketch time against 1 wavefront / clk / SM
+                wf_peak = 148 * sm_max * 1e6
+                roof["smem"] = {"wavefronts_per_launch": tr["smem_wavefronts"],
+                                "frac": tr["smem_wavefronts"] / (t_sk * 1e-3) / wf_peak,
+                                "peak": "148 SMs x 1 wavefront (128 B) / clk x sm_max_mhz"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             krows = (lambda rows: pts[torch.as_tensor(rows, device=dev) - rb][:, :n].double().cpu().numpy()) \
