@@ -148,7 +148,12 @@ typedef struct ks_tsqr_plan* ks_tsqr_handle;
  * eq. (5) (the running R absorbs one block R per step).  R is the same (unique). */
 /* KS_TSQR_MIXED: eq. (5) exactly as printed -- the blocks in two halves, a chain inside each half (advancing
  * side by side), then one merge of the two chains' R's: the paper's "mixture of the strategies". */
-typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1, KS_TSQR_MIXED = 2 } ks_tsqr_topology;
+/* KS_TSQR_TRIANGULAR (a flag OR-ed into the topology): every block is exactly d rows and upper triangular -- a
+ * stack of R factors, the second TSQR level (eqs. (2)-(3), :252).  Rows below a block's
+ * diagonal are zero, so in panel k only its first 32 (k + 1) rows take part (the reflectors act as the identity
+ * on the rest): the same R, less work and latency for the early panels.  Needs rows == blocks * d, d <= 512;
+ * ks_tsqr_merge uses it (with the pairwise tree over the P stacked R's). */
+typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1, KS_TSQR_MIXED = 2, KS_TSQR_TRIANGULAR = 16 } ks_tsqr_topology;
 
 KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks, size_t* bytes);
 KS_API ks_status ks_tsqr_workspace_size_ex(int64_t rows, int32_t d, int32_t blocks, int32_t topology, size_t* bytes);

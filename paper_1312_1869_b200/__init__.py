@@ -20,7 +20,7 @@ import torch
 __all__ = [
     "KsError", "SketchDesc", "SQEXP", "MATERN32", "STORED", "ks_sketch_stored", "SRHT", "GAUSS", "DHT", "DCT", "lib", "library_path",
     "ks_sketch_workspace_size", "ks_sketch", "ks_omega_export", "ks_omega_apply",
-    "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr_work_matrix", "ks_tsqr", "ks_qform", "TSQR_TREE", "TSQR_CHAIN", "TSQR_MIXED",
+    "ks_tsqr_workspace_size", "ks_tsqr_create", "ks_tsqr_destroy", "ks_tsqr_work_matrix", "ks_tsqr", "ks_qform", "TSQR_TREE", "TSQR_CHAIN", "TSQR_MIXED", "TSQR_TRIANGULAR",
     "ks_tsqr_workspace_size_ex", "ks_tsqr_create_ex", "ks_tsqr_apply_qt", "ks_tsqr_apply_q",
     "ks_tsqr_merge_workspace_size", "ks_tsqr_merge", "ks_apply_qt_workspace_size", "ks_apply_qt",
     "ks_apply_q", "ks_trsolve", "ks_lowrank_workspace_size", "ks_lowrank_solve", "ks_last_error",
@@ -199,6 +199,7 @@ def ks_tsqr_create(rows, d, blocks, ws) -> C.c_void_p:
 
 
 TSQR_TREE, TSQR_CHAIN, TSQR_MIXED = 0, 1, 2
+TSQR_TRIANGULAR = 16   # flag: the blocks are d x d upper-triangular R's (the second TSQR level)
 
 
 def ks_tsqr_workspace_size_ex(rows, d, blocks, topology) -> int:

@@ -123,7 +123,7 @@ size_t dense_apply_ws(const ks_sketch_desc& D);
 void tsqr_set_graphs(ks_tsqr_handle h, bool on);
 // ks_tsqr_create with the plan metadata uploaded stream-ordered on st (one-shot plans).
 ks_status tsqr_create_on_stream(int64_t rows, int32_t d, int32_t blocks, void* ws, size_t ws_bytes,
-                                ks_tsqr_handle* out, cudaStream_t st);
+                                ks_tsqr_handle* out, cudaStream_t st, int32_t topology = KS_TSQR_TREE);
 
 // ---------------------------------------------------------------- solve side
 // NEXT-4 (ks_gp.cu)

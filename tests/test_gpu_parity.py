@@ -494,3 +494,28 @@ def test_one_shot_strict_solve_and_alignment_errors(ks, cuda):
     with pytest.raises(ks.KsError) as e:
         ks.ks_sketch(desc, _t(pts, cuda), 0, n, buf[1:].view(n, d), sk.ws)
     assert e.value.status == 1 and "aligned" in str(e.value)
+
+
+@pytest.mark.parametrize("P,d", [(2, 64), (8, 512), (4, 256), (3, 100), (8, 36)])
+def test_tsqr_merge_of_triangular_stack(ks, cuda, P, d):
+    """The second TSQR level (eqs. (2)-(3)): ks_tsqr_merge of P stacked upper-triangular R's runs
+    the pairwise tree with KS_TSQR_TRIANGULAR (rows below each R's diagonal skipped, panel by panel).  R against
+    the oracle's flat Householder QR of the stack, Q2 R = stack, Q2^T Q2 = I."""
+    import torch
+    rng = np.random.default_rng(P * 1000 + d)
+    Rs = []
+    for p in range(P):   # genuine R factors: QR of random tall blocks, graded like a sketch's R
+        M = rng.standard_normal((2 * d, d)) * np.exp(-np.arange(d) / (d / 4.0))
+        Rs.append(np.linalg.qr(M, mode="r"))
+    stack = np.concatenate(Rs, 0).astype(np.float32)
+    Q2 = torch.empty((P * d, d), device=cuda)
+    R = torch.empty((d, d), device=cuda)
+    ws = torch.empty(ks.ks_tsqr_merge_workspace_size(P, d), dtype=torch.uint8, device=cuda)
+    ks.ks_tsqr_merge(_t(stack, cuda), P, d, Q2, R, ws)
+    torch.cuda.synchronize()
+    Rn, Qn = R.cpu().numpy().astype(np.float64), Q2.cpu().numpy().astype(np.float64)
+    _, Rr = oracle.householder_qr(stack.astype(np.float64), want_q=False)
+    assert np.all(np.tril(Rn, -1) == 0) and np.all(np.diag(Rn) >= 0)
+    assert relF(align_rows(Rn, Rr), Rr) <= R_TOL
+    assert relF(Qn @ Rn, stack) <= 1e-5
+    assert np.linalg.norm(Qn.T @ Qn - np.eye(d)) <= 1e-4 * np.sqrt(d)
