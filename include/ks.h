@@ -151,8 +151,8 @@ typedef struct ks_tsqr_plan* ks_tsqr_handle;
 /* KS_TSQR_TRIANGULAR (a flag OR-ed into the topology): every block is exactly d rows and upper triangular -- a
  * stack of R factors, the second TSQR level (eqs. (2)-(3), :252).  Rows below a block's
  * diagonal are zero, so in panel k only its first 32 (k + 1) rows take part (the reflectors act as the identity
- * on the rest): the same R, less work and latency for the early panels.  Needs rows == blocks * d, d <= 512;
- * ks_tsqr_merge uses it (with the pairwise tree over the P stacked R's). */
+ * on the rest): the same R, less work and latency for the early panels.  Needs rows a multiple of d, whole R's
+ * per block, d <= 512 (every R is its own leaf); ks_tsqr_merge uses it (one block: a flat merge of the P R's). */
 typedef enum { KS_TSQR_TREE = 0, KS_TSQR_CHAIN = 1, KS_TSQR_MIXED = 2, KS_TSQR_TRIANGULAR = 16 } ks_tsqr_topology;
 
 KS_API ks_status ks_tsqr_workspace_size(int64_t rows, int32_t d, int32_t blocks, size_t* bytes);

@@ -69,13 +69,13 @@ class CudaOps:
         f32 = dict(dtype=torch.float32, device=self.device)
         self.sk = Sketch(self.desc, self.device)
         self.plan = TsqrPlan(rows, d, blocks_per_rank, self.device)
-        # the second level: the QR of the stacked R's -- the pairwise tree over the P triangular
-        # R's (eqs. (2)-(3), KS_TSQR_TRIANGULAR: rows below each R's diagonal skipped), as ks_tsqr_merge
+        # the second level: the QR of the stacked R's, as ks_tsqr_merge -- one block whose leaves
+        # are the P triangular R's (KS_TSQR_TRIANGULAR: rows below each diagonal skipped), one flat merge level
         from . import TSQR_TREE, TSQR_TRIANGULAR
         self.mplan = None
         if world > 1:
-            self.mplan = (TsqrPlan(world * d, d, world, self.device, topology=TSQR_TREE | TSQR_TRIANGULAR) if d <= 512
-                          else TsqrPlan(world * d, d, 1, self.device))
+            tri = d <= 512 and world * d > 512   # (a stack of <= 512 rows is a single leaf: no merge level)
+            self.mplan = TsqrPlan(world * d, d, 1, self.device, topology=TSQR_TREE | (TSQR_TRIANGULAR if tri else 0))
         # inplace: the sketch goes straight into the TSQR plan's working matrix (no rows x d copy, one
         # rows x d buffer less); Y is then consumed by the factorisation
         self.Y = self.plan.work_matrix() if inplace else torch.empty((rows, d), **f32)

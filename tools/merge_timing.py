@@ -20,7 +20,8 @@ for d in (512, 256):
         Q2 = torch.empty_like(S)
         R = torch.empty((d, d), device=dev)
         line = f"d={d} P={P}:"
-        for name, blocks, topo in (("flat", 1, ks.TSQR_TREE), ("pairwise-tri", P, ks.TSQR_TREE | ks.TSQR_TRIANGULAR),
+        for name, blocks, topo in (("flat", 1, ks.TSQR_TREE), ("flat-tri", 1, ks.TSQR_TREE | ks.TSQR_TRIANGULAR),
+                                   ("pairwise-tri", P, ks.TSQR_TREE | ks.TSQR_TRIANGULAR),
                                    ("pairwise", P, ks.TSQR_TREE)):
             plan = ks.TsqrPlan(P * d, d, blocks, dev, topology=topo)
             for _ in range(3):
