@@ -103,7 +103,8 @@ def test_sketch_full_config_sampled_rows(ks, cuda, name, nrows):
 # ---------------------------------------------------------------- TSQR
 TSQR_CASES = [(2048, 64, 4), (16384, 128, 8), (4096, 256, 16), (8192, 512, 8), (3000, 100, 3), (700, 33, 5),
               (512, 512, 1), (530, 512, 1), (40000, 64, 3),   # (530, 512, 1): one 530-row leaf (512-thread QR)
-              (4096, 100, 8), (8192, 36, 16)]   # TMA leaf apply (512-row leaves) with a partial last panel (w = 4)
+              (4096, 100, 8), (8192, 36, 16),   # TMA leaf apply (512-row leaves) with a partial last panel (w = 4)
+              (8192, 200, 4), (16384, 300, 8)]  # tcgen05 leaf apply with partial 128-column tiles and panels
 
 
 @pytest.mark.parametrize("rows,d,blocks", TSQR_CASES)
@@ -139,7 +140,8 @@ def test_tsqr_chain_topology_matches_oracle_chain(ks, cuda, rows, d, blocks, cha
 
 
 @pytest.mark.parametrize("rows,d,blocks,m,topology", [(8192, 128, 8, 16, 0), (4096, 64, 4, 5, 0), (3000, 100, 3, 8, 1),
-                                                       (65536, 256, 16, 32, 0)])
+                                                       (65536, 256, 16, 32, 0),
+                                                       (8192, 96, 4, 160, 0)])   # m = 160: tcgen05 tiles of X
 def test_tsqr_implicit_q_applies(ks, cuda, rows, d, blocks, m, topology):
     """Implicit Q: Q^T A from the stored reflectors.  Pinned by Y^T A = R^T (Q^T A) in fp64
     (independent of the explicit Q) and against the explicit Q; Q C likewise."""
