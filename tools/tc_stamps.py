@@ -42,6 +42,9 @@ try:
     w = np.frombuffer(buf, dtype=np.uint64)[1 << 19:(1 << 19) + 264 * 64].reshape(264, 32, 2).astype(np.int64)
     wv = w[valid]
     print(f"pass-1 waits per item (us): conv-slot / MMA done + drain {wv[:, 0].mean() / 1e3:.2f}, ring full {wv[:, 1].mean() / 1e3:.2f}")
+    x = np.frombuffer(buf, dtype=np.uint64)[3 << 18:(3 << 18) + 264 * 128].reshape(264, 32, 4).astype(np.int64)[valid]
+    print(f"pass-1 work per item (us): A conversion {x[:, 0].mean() / 1e3:.2f}, B conversion {x[:, 1].mean() / 1e3:.2f}, "
+          f"fences + arrive {x[:, 2].mean() / 1e3:.2f}")
     print("items per CTA:", np.bincount(valid.sum(1))[np.bincount(valid.sum(1)) > 0], "(counts of CTAs by items)")
 finally:
     shutil.copy("/tmp/ks_keep.so", lib_path + ".tmp")
