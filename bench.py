@@ -254,6 +254,7 @@ def run_ours(args, cfg, pts_np, A_np):
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # keep stdout to the one JSON line
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
@@ -498,8 +499,9 @@ def relaunch_distributed(args):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")          # the NCCL init lines show every rank joining
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG", "INFO")          # the NCCL init lines show every rank joining (on stderr:
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")   # stdout carries only rank 0's JSON line)
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
     os.execvpe(sys.executable, cmd, env)
