@@ -32,7 +32,11 @@
 namespace ks {
 
 constexpr int kGaussSegKb = 16;   // 1024 columns of K per TMEM accumulation segment
-constexpr int kGThreads = 512;
+#ifndef KS_GAUSS_DRAINERS
+#define KS_GAUSS_DRAINERS 4   // drainer warps per CTA (4 or 8); 8 measured slower: c3 sketch 3.544 vs 3.492 ms
+#endif
+constexpr int kGDrainWarps = KS_GAUSS_DRAINERS;
+constexpr int kGThreads = 384 + 32 * kGDrainWarps;
 constexpr int kATileBytes = kGaussBM * kGaussBK * 2;  // 16 KB per fp16 half
 
 KS_DEVINL uint32_t pack_half2(float a, float b) {
@@ -249,7 +253,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(accf0 + 8 * b, 1);
-      mbar_init(acce0 + 8 * b, 8);         // 4 drain warps x 2 CTAs
+      mbar_init(acce0 + 8 * b, 2 * kGDrainWarps);   // the drain warps of both CTAs
     }
     for (int s = 0; s < kPtsStages; ++s) {
       mbar_init(pfull0 + 8 * s, 1);
@@ -380,17 +384,19 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
   } else if (warp >= 12) {
     // ---------------- drainers: running sum (TMEM columns [DN, 2 DN)) += segment accumulator (columns
     // [0, DN)), added in fp32 round-to-nearest on the CUDA cores; the last segment is scaled and stored.
-    const int quarter = warp & 3;
+    // (with 8 drain warps, two per lane quarter, each folds half of the columns: the MMA waits for the drain)
+    const int quarter = warp & 3, dpart = (warp - 12) >> 2, nparts = kGDrainWarps / 4;
     const int row = 32 * quarter + lane;
     const int64_t i = row0 + row;
     const bool ok = i < row_end;
     float* yr = Y + (i - row_begin) * (int64_t)DN;
     const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
+    const int cb = 16 * ((DN / 16) * dpart / nparts), ce = 16 * ((DN / 16) * (dpart + 1) / nparts);   // 16-col units
     for (int g = 0; g < nseg; ++g) {
       mbar_wait(accf0, g & 1);
       tc_fence_after();
       const bool first = g == 0, last = g == nseg - 1;
-      for (int c0 = 0; c0 < DN; c0 += 16) {
+      for (int c0 = cb; c0 < ce; c0 += 16) {
         float v[16];
         tmem_ld16(tl + (uint32_t)c0, v);
         if (!first) {
