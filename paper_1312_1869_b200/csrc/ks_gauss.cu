@@ -368,8 +368,10 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       float4 pts[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) pts[q] = lds128(smem_u32(pring + ps * kGaussBK + 8 * cq + (q ^ cq)));
+#ifdef KS_GAUSS_EARLY_PEMPTY   // (study only: releases the slot while the LDS may still be in flight)
       __syncwarp();
-      if (lane == 0) mbar_arrive(pempty0 + 8 * ps);   // release: this warp's reads of the slot are done
+      if (lane == 0) mbar_arrive(pempty0 + 8 * ps);
+#endif
       mbar_wait(empty0 + 8 * s, ph ^ 1);
       const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
       if constexpr (KIND == KS_KERNEL_STORED) {
@@ -379,7 +381,14 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
         produce_tile<DIM, KIND>(xi2, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(rank == 0 ? full0 + 8 * s : lfull0 + 8 * s);
+      if (lane == 0) {
+        mbar_arrive(rank == 0 ? full0 + 8 * s : lfull0 + 8 * s);
+#ifndef KS_GAUSS_EARLY_PEMPTY
+        // the points slot is released only once its values have been consumed (the tile above used them),
+        // so no shared load of the slot can still be in flight when the loader's TMA refills it
+        mbar_arrive(pempty0 + 8 * ps);
+#endif
+      }
     }
   } else if (warp >= 12) {
     // ---------------- drainers: running sum (TMEM columns [DN, 2 DN)) += segment accumulator (columns
