@@ -36,6 +36,10 @@ constexpr int kGaussSegKb = 16;   // 1024 columns of K per TMEM accumulation seg
 #define KS_GAUSS_DRAINERS 4   // drainer warps per CTA (4 or 8); 8 measured slower: c3 sketch 3.544 vs 3.492 ms
 #endif
 constexpr int kGDrainWarps = KS_GAUSS_DRAINERS;
+#ifndef KS_GAUSS_DRAIN_U
+#define KS_GAUSS_DRAIN_U 2   // 16-column TMEM loads in flight per drainer step
+#endif
+constexpr int kDrainU = KS_GAUSS_DRAIN_U;
 constexpr int kGThreads = 384 + 32 * kGDrainWarps;
 constexpr int kATileBytes = kGaussBM * kGaussBK * 2;  // 16 KB per fp16 half
 
@@ -142,6 +146,45 @@ KS_DEVINL void produce_tile_stored(const float (&kv)[4][8], const int64_t (&irow
       const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
       sts128(smem_u32(a_hi + off), hi[h][0], hi[h][1], hi[h][2], hi[h][3]);
       sts128(smem_u32(a_lo + off), lo[h][0], lo[h][1], lo[h][2], lo[h][3]);
+    }
+  }
+}
+
+// Drainer step over 16 U columns of this warp's 32 TMEM lanes: running sum (columns DN + c) += segment
+// accumulator (columns c), fp32 round-to-nearest; the last segment scales and stores the row of Y.  All
+// loads of the step are in flight together (one tcgen05.wait::ld), so a segment boundary -- where the MMA
+// waits for the drain -- costs one TMEM round trip per 16 U columns instead of two per 16.
+template <int U>
+KS_DEVINL void drain_cols(uint32_t tl, int DN, int c0, bool first, bool last, bool ok, float* yr, float out_scale) {
+  uint32_t a[U][16], b[U][16];
+#pragma unroll
+  for (int u = 0; u < U; ++u) tmem_ld16_issue(tl + (uint32_t)(c0 + 16 * u), a[u]);
+  if (!first) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) tmem_ld16_issue(tl + (uint32_t)(DN + c0 + 16 * u), b[u]);
+  }
+  tmem_wait_ld();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    tmem_pin16(a[u]);
+    float v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(a[u][q]);
+    if (!first) {
+      tmem_pin16(b[u]);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] += __uint_as_float(b[u][q]);
+    }
+    if (last) {
+      if (ok) {
+        float4* dst = reinterpret_cast<float4*>(yr + c0 + 16 * u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[q] = make_float4(v[4 * q] * out_scale, v[4 * q + 1] * out_scale, v[4 * q + 2] * out_scale,
+                               v[4 * q + 3] * out_scale);
+      }
+    } else {
+      tmem_st16(tl + (uint32_t)(DN + c0 + 16 * u), v);
     }
   }
 }
@@ -405,27 +448,9 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       mbar_wait(accf0, g & 1);
       tc_fence_after();
       const bool first = g == 0, last = g == nseg - 1;
-      for (int c0 = cb; c0 < ce; c0 += 16) {
-        float v[16];
-        tmem_ld16(tl + (uint32_t)c0, v);
-        if (!first) {
-          float u[16];
-          tmem_ld16(tl + (uint32_t)(DN + c0), u);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] += u[q];
-        }
-        if (last) {
-          if (ok) {
-            float4* dst = reinterpret_cast<float4*>(yr + c0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              dst[q] = make_float4(v[4 * q] * out_scale, v[4 * q + 1] * out_scale, v[4 * q + 2] * out_scale,
-                                   v[4 * q + 3] * out_scale);
-          }
-        } else {
-          tmem_st16(tl + (uint32_t)(DN + c0), v);
-        }
-      }
+      int c0 = cb;
+      for (; c0 + 16 * kDrainU <= ce; c0 += 16 * kDrainU) drain_cols<kDrainU>(tl, DN, c0, first, last, ok, yr, out_scale);
+      for (; c0 < ce; c0 += 16) drain_cols<1>(tl, DN, c0, first, last, ok, yr, out_scale);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();

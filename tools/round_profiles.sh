@@ -10,7 +10,7 @@ timeout 900 python bench.py --steps 5 --warmup 3 > $out/bench_default.log 2>&1; 
 for c in ${CONFIGS:-c1 c2 c3 c4 c5}; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_$c.log 2>&1
 done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches_c4.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file $out/launches_c4.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $out/ncu_launch.log 2>&1
 python tools/launches.py $out/launches_c4.csv > $out/launches_c4.txt 2>&1
 NCU="ncu --clock-control none --set full --import-source on"
