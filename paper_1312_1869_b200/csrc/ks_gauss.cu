@@ -40,7 +40,13 @@ constexpr int kGDrainWarps = KS_GAUSS_DRAINERS;
 #define KS_GAUSS_DRAIN_U 2   // 16-column TMEM loads in flight per drainer step
 #endif
 constexpr int kDrainU = KS_GAUSS_DRAIN_U;
-constexpr int kGThreads = 384 + 32 * kGDrainWarps;
+#ifndef KS_GAUSS_PRODUCERS
+#define KS_GAUSS_PRODUCERS 8   // K-tile producer warps per CTA (8: 4 rows per thread; 16: 2 rows per thread)
+#endif
+constexpr int kGProdWarps = KS_GAUSS_PRODUCERS;
+constexpr int kGRowsPT = 128 / (4 * kGProdWarps);   // rows per producer thread (8 column groups of 8)
+static_assert(kGRowsPT == 2 || kGRowsPT == 4, "8 or 16 producer warps");
+constexpr int kGThreads = 128 + 32 * kGProdWarps + 32 * kGDrainWarps;
 constexpr int kATileBytes = kGaussBM * kGaussBK * 2;  // 16 KB per fp16 half
 
 KS_DEVINL uint32_t pack_half2(float a, float b) {
@@ -54,10 +60,10 @@ KS_DEVINL uint32_t pack_half2(float a, float b) {
 // S*K, split hi/lo and stored in the UMMA K-major SW128 layout.  The covariance and the lo = x - hi
 // subtraction run on packed f32x2 row pairs (one issue slot per two rows).
 template <int DIM, int KIND>
-KS_DEVINL void produce_tile(const f2_t (&xi2)[2][3], const int64_t (&irow)[4], const float4 (&pts)[8], int64_t j0,
-                            bool diag, float nugget, uint8_t* a_hi, uint8_t* a_lo, int rq, int cq) {
+KS_DEVINL void produce_tile(const f2_t (&xi2)[kGRowsPT / 2][3], const int64_t (&irow)[kGRowsPT], const float4 (&pts)[8],
+                            int64_t j0, bool diag, float nugget, uint8_t* a_hi, uint8_t* a_lo, int rq, int cq) {
 #pragma unroll
-  for (int pr = 0; pr < 2; ++pr) {
+  for (int pr = 0; pr < kGRowsPT / 2; ++pr) {
     f2_t v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = cov_signed2<DIM, KIND>(xi2[pr], pts[q]);
@@ -85,7 +91,7 @@ KS_DEVINL void produce_tile(const f2_t (&xi2)[2][3], const int64_t (&irow)[4], c
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = 4 * rq + 2 * pr + h;
+      const int r = kGRowsPT * rq + 2 * pr + h;
       const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
       sts128(smem_u32(a_hi + off), hi[h][0], hi[h][1], hi[h][2], hi[h][3]);   // st.shared: the tile pointers
       sts128(smem_u32(a_lo + off), lo[h][0], lo[h][1], lo[h][2], lo[h][3]);   // are generic (aligned base)
@@ -96,10 +102,10 @@ KS_DEVINL void produce_tile(const f2_t (&xi2)[2][3], const int64_t (&irow)[4], c
 // Stored K (NEXT-2): the same tile from K in HBM, v = K[i][j] * a_j (a_j = S), no evaluation.  The loads
 // of the next stage are issued right after this stage's tile is stored (load_tile_stored), so they are in
 // flight while the producer waits on the ring barriers.
-KS_DEVINL void load_tile_stored(const float* __restrict__ Kst, int64_t ldk, int64_t ncols, const int64_t (&irow)[4],
-                                int64_t row_last, int64_t j0, float (&kv)[4][8]) {
+KS_DEVINL void load_tile_stored(const float* __restrict__ Kst, int64_t ldk, int64_t ncols, const int64_t (&irow)[kGRowsPT],
+                                int64_t row_last, int64_t j0, float (&kv)[kGRowsPT][8]) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+  for (int r = 0; r < kGRowsPT; ++r) {
     const float* kr = Kst + (irow[r] <= row_last ? irow[r] : row_last) * ldk + j0;
     if (j0 + 8 <= ncols) {
       const float4 a = __ldg(reinterpret_cast<const float4*>(kr)), b = __ldg(reinterpret_cast<const float4*>(kr + 4));
@@ -111,10 +117,10 @@ KS_DEVINL void load_tile_stored(const float* __restrict__ Kst, int64_t ldk, int6
     }
   }
 }
-KS_DEVINL void produce_tile_stored(const float (&kv)[4][8], const int64_t (&irow)[4], const float4 (&pts)[8],
+KS_DEVINL void produce_tile_stored(const float (&kv)[kGRowsPT][8], const int64_t (&irow)[kGRowsPT], const float4 (&pts)[8],
                                    int64_t j0, bool diag, float nugget, uint8_t* a_hi, uint8_t* a_lo, int rq, int cq) {
 #pragma unroll
-  for (int pr = 0; pr < 2; ++pr) {
+  for (int pr = 0; pr < kGRowsPT / 2; ++pr) {
     f2_t v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = f2mul(f2(kv[2 * pr][q], kv[2 * pr + 1][q]), f2s(pts[q].w));
@@ -142,7 +148,7 @@ KS_DEVINL void produce_tile_stored(const float (&kv)[4][8], const int64_t (&irow
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = 4 * rq + 2 * pr + h;
+      const int r = kGRowsPT * rq + 2 * pr + h;
       const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(cq ^ (r & 7)) << 4);
       sts128(smem_u32(a_hi + off), hi[h][0], hi[h][1], hi[h][2], hi[h][3]);
       sts128(smem_u32(a_lo + off), lo[h][0], lo[h][1], lo[h][2], lo[h][3]);
@@ -290,8 +296,8 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < NST; ++s) {
-      mbar_init(full0 + 8 * s, 8 + 1 + 1);   // leader's 8 producer warps + the peer's relay + expect_tx
-      mbar_init(lfull0 + 8 * s, 8);           // peer: its 8 producer warps (relayed to the leader)
+      mbar_init(full0 + 8 * s, kGProdWarps + 1 + 1);   // leader's producer warps + the peer's relay + expect_tx
+      mbar_init(lfull0 + 8 * s, kGProdWarps);           // peer: its producer warps (relayed to the leader)
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -300,7 +306,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
     }
     for (int s = 0; s < kPtsStages; ++s) {
       mbar_init(pfull0 + 8 * s, 1);
-      mbar_init(pempty0 + 8 * s, 8);       // the 8 producer warps of this CTA
+      mbar_init(pempty0 + 8 * s, kGProdWarps);   // the producer warps of this CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -322,6 +328,10 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
         const int s = kb % NST;
         const uint32_t ph = (kb / NST) & 1;
         mbar_wait(empty0 + 8 * s, ph ^ 1);
+        if (dbg & 4) {   // timing study only (wrong results): bit 2 skips the Omega tile loads
+          if (rank == 0) mbar_arrive(full0 + 8 * s);
+          continue;
+        }
         if (rank == 0) mbar_arrive_tx(full0 + 8 * s, 2 * kBStage);
         tma_load_2d_2cta(smem_u32(b_t + s * kBStage), &tmB, (kb0 + kb) * kGaussBK, (int)rank * (DN / 2),
                          full0_L + 8 * s);
@@ -338,7 +348,11 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % NST;
         mbar_wait(lfull0 + 8 * s, (kb / NST) & 1);
+#ifdef KS_GAUSS_RELAY_RELAXED   // timing study only: no cluster-scope release (unsafe with real tiles)
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(full0_L + 8 * s) : "memory");
+#else
         asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(full0_L + 8 * s) : "memory");
+#endif
       }
     }
   } else if (warp == 2) {
@@ -381,18 +395,18 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
         umma_commit_2cta(accf0);
       }
     }
-  } else if (warp >= 4 && warp < 12) {
-    // ---------------- K-tile producers: thread p -> rows 4rq..4rq+3, columns 8cq..8cq+7 of the tile
+  } else if (warp >= 4 && warp < 4 + kGProdWarps) {
+    // ---------------- K-tile producers: thread p -> rows kGRowsPT rq .. + kGRowsPT - 1, columns 8cq..8cq+7
     const int p = threadIdx.x - 128;
     const int rq = p >> 3, cq = p & 7;
-    f2_t xi2[2][3];
-    int64_t irow[4];
+    f2_t xi2[kGRowsPT / 2][3];
+    int64_t irow[kGRowsPT];
 #pragma unroll
-    for (int pr = 0; pr < 2; ++pr) {
+    for (int pr = 0; pr < kGRowsPT / 2; ++pr) {
       float4 q[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int64_t i = row0 + 4 * rq + 2 * pr + h;
+        int64_t i = row0 + kGRowsPT * rq + 2 * pr + h;
         irow[2 * pr + h] = i;
         if (i >= row_end) i = row_end - 1;
         q[h] = pk[i];
@@ -400,7 +414,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       xi2[pr][0] = f2(q[0].x, q[1].x); xi2[pr][1] = f2(q[0].y, q[1].y); xi2[pr][2] = f2(q[0].z, q[1].z);
     }
     const float* Kb = Kst - row_begin * ldk;   // (stored K: row i at Kb + i * ldk)
-    float kv[4][8];
+    float kv[kGRowsPT][8];
     if constexpr (KIND == KS_KERNEL_STORED) load_tile_stored(Kb, ldk, ncols, irow, row_end - 1, (int64_t)kb0 * kGaussBK + 8 * cq, kv);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % NST;
@@ -416,7 +430,7 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
       if (lane == 0) mbar_arrive(pempty0 + 8 * ps);
 #endif
       mbar_wait(empty0 + 8 * s, ph ^ 1);
-      const bool diag = (j0 + 8 > row0 + 4 * rq) && (j0 < row0 + 4 * rq + 4);
+      const bool diag = (j0 + 8 > row0 + kGRowsPT * rq) && (j0 < row0 + kGRowsPT * rq + kGRowsPT);
       if constexpr (KIND == KS_KERNEL_STORED) {
         produce_tile_stored(kv, irow, pts, j0, diag, nugget, a_hi + s * kATileBytes, a_lo + s * kATileBytes, rq, cq);
         if (kb + 1 < nkb) load_tile_stored(Kb, ldk, ncols, irow, row_end - 1, j0 + kGaussBK, kv);
@@ -433,11 +447,11 @@ k_sketch_gauss2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__
 #endif
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 4 + kGProdWarps) {
     // ---------------- drainers: running sum (TMEM columns [DN, 2 DN)) += segment accumulator (columns
     // [0, DN)), added in fp32 round-to-nearest on the CUDA cores; the last segment is scaled and stored.
     // (with 8 drain warps, two per lane quarter, each folds half of the columns: the MMA waits for the drain)
-    const int quarter = warp & 3, dpart = (warp - 12) >> 2, nparts = kGDrainWarps / 4;
+    const int quarter = warp & 3, dpart = (warp - 4 - kGProdWarps) >> 2, nparts = kGDrainWarps / 4;
     const int row = 32 * quarter + lane;
     const int64_t i = row0 + row;
     const bool ok = i < row_end;
