@@ -19,6 +19,15 @@ KS_DEVINL void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
 KS_DEVINL void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok) {
+#ifdef KS_MBAR_NO_HINT   // (study: plain try_wait polling)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -26,6 +35,7 @@ KS_DEVINL void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(bar), "r"(parity), "r"(0x989680u)
         : "memory");
+#endif
   }
 }
 KS_DEVINL void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
